@@ -1,0 +1,403 @@
+// K3 -- fused Fastfood expansion (replaces fastfood.py:179-226:
+// apply_zhat_batch + feature_map_batch).
+//
+// One thread group (T threads, R = n/T values each) owns one input row.  The
+// row is read once from HBM (16-byte loads, zero padding implicit) and kept
+// in registers for all E blocks.  Per block:
+//   x*B  : sign-bit XOR from a per-thread mask word          (fastfood.py:190)
+//   H    : register butterflies + shared-memory exchanges     (:191)
+//   Pi,G : one scatter into shared memory: z1[j] goes to perm^-1[j] already
+//          multiplied by g[perm^-1[j]] (the same fp32 product the reference
+//          forms after its gather, :192-193)
+//   H    : middle rounds first, ending in the 16-byte store layout (:194)
+//   C*s  : one multiply when 1/(sigma*sqrt n) is a power of two (exactly the
+//          reference's two roundings), else two               (:195-196)
+//   cos/sin epilogue with 2*pi range reduction, [cos | sin] halves, optional
+//          float32(1/sqrt(D)) (:220-225); 16-byte stores.
+// HBM traffic is one read of x and one write of the features.
+//
+// The `parity` variant restates the reference arithmetic exactly (sequential
+// base-256 sums, (a+b)-2b combine, separate roundings) for bit-exact z checks.
+#include "mck_common.cuh"
+#include "fwht_core.cuh"
+#include "tables.cuh"
+
+namespace mck {
+
+template <class C>
+constexpr int ff_rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
+
+// ---------------------------------------------------------------- derived tables
+__global__ void k_perminv(const int32_t* perm, int64_t n, int32_t E, int32_t* perminv,
+                          int32_t* flag) {
+  const int64_t total = n * E;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / n, i = t % n;
+    const int32_t j = perm[t];
+    if (j < 0 || j >= n) {
+      atomicExch(flag, 1);
+      continue;
+    }
+    perminv[e * n + j] = (int32_t)i;
+  }
+}
+
+__global__ void k_perm_check(const int32_t* perm, const int32_t* perminv, int64_t n, int32_t E,
+                             int32_t* flag) {
+  const int64_t total = n * E;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / n, j = t % n;
+    const int32_t i = perminv[t];
+    if (i < 0 || i >= n || perm[e * n + i] != (int32_t)j) atomicExch(flag, 1);
+  }
+}
+
+__global__ void k_cscale(const float* c, int64_t total, float scale, int fold, float* cs) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x)
+    cs[t] = fold ? c[t] * scale : c[t];
+}
+
+// Sign masks (layout L) and scatter entries (layout of H1's last round).
+template <class C>
+__global__ void k_prepare(const float* b, const float* g, const int32_t* perminv, int32_t E,
+                          uint32_t* bmask, uint2* scat) {
+  constexpr int R = C::R, T = C::T, W = (R + 31) / 32;
+  constexpr uint32_t PM = last_mid_regs<C>();
+  const int64_t total = (int64_t)E * R * T;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / (R * T);
+    const int k = (int)((t / T) % R);
+    const uint32_t tid = (uint32_t)(t % T);
+    const int64_t off = e * (int64_t)C::N;
+    const uint32_t j = lay_index<PM>(thread_part<C::FULL, PM>(tid), k);
+    const int32_t pinv = perminv[off + j];
+    scat[t] = make_uint2(pad_addr((uint32_t)pinv), __float_as_uint(g[off + pinv]));
+    if (k < W) {
+      uint32_t bits = 0;
+      for (int q = 0; q < 32 && 32 * k + q < R; ++q) {
+        const uint32_t i = lay_index<C::PL>(thread_part<C::FULL, C::PL>(tid), 32 * k + q);
+        if (b[off + i] < 0.0f) bits |= 1u << q;
+      }
+      bmask[(e * W + k) * T + tid] = bits;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- sincos
+__device__ __forceinline__ void sincos_fast(float z, float& s, float& c) {
+  const float k = rintf(z * 0.159154943091895336f);
+  float r = fmaf(-k, 6.28318548202514648f, z);
+  r = fmaf(-k, -1.74845553146951720e-7f, r);
+  __sincosf(r, &s, &c);
+}
+
+struct FFParams {
+  const float* x;
+  int64_t m;
+  int64_t ldx;
+  int32_t d;
+  const int32_t* rows;
+  const uint32_t* bmask;
+  const uint2* scat;
+  const float* cs;
+  float scale;
+  float norm;
+  float* out;
+  int64_t ldo;
+  int32_t E;
+  int64_t D;
+};
+
+template <class C, bool FEAT, bool FOLD, bool VEC>
+__global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>())
+k_fastfood(FFParams p) {
+  constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
+  constexpr int ROWS = ff_rows_per_cta<C>();
+  extern __shared__ __align__(16) float ff_smem[];
+  const int gid = threadIdx.x / T;
+  const uint32_t tid = threadIdx.x % T;
+  float* s = ff_smem + gid * C::SMEM_FLOATS;
+  const int64_t row = (int64_t)blockIdx.x * ROWS + gid;
+  const bool valid = row < p.m;
+
+  // ---- input row, layout L, zero padded
+  float xr[R];
+  {
+    const int64_t src = valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0;
+    const float* xp = p.x + src * p.ldx;
+#pragma unroll
+    for (int j = 0; j < R / 4; ++j) {
+      const int i0 = 4 * (int)tid + j * 4 * T;
+      if constexpr (VEC) {
+        float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && i0 < p.d) t4 = __ldg(reinterpret_cast<const float4*>(xp + i0));
+        xr[4 * j] = t4.x; xr[4 * j + 1] = t4.y; xr[4 * j + 2] = t4.z; xr[4 * j + 3] = t4.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) xr[4 * j + c] = (valid && i0 + c < p.d) ? __ldg(xp + i0 + c) : 0.f;
+      }
+    }
+  }
+  constexpr uint32_t P0 = C::mid_regs(0);
+  float* orow = p.out + (valid ? row : 0) * p.ldo;
+
+  for (int e = 0; e < p.E; ++e) {
+    float v[R];
+    // ---- x * B (sign XOR, exact)
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const uint32_t bits = __ldg(p.bmask + ((int64_t)e * W + w) * T + tid);
+#pragma unroll
+      for (int q = 0; q < 32 && 32 * w + q < R; ++q)
+        v[32 * w + q] = __uint_as_float(__float_as_uint(xr[32 * w + q]) ^ (((bits >> q) & 1u) << 31));
+    }
+    // ---- H (first)
+    butterflies<R, C::PL, C::PL>(v);
+    middle_rounds<C, 0, C::PL>(s, tid, gid, v);
+    // ---- Pi and G: scatter z1[j] * g[perm^-1[j]] to perm^-1[j]
+    {
+      const uint2* sc = p.scat + (int64_t)e * R * T + tid;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const uint2 a = __ldg(sc + k * T);
+        s[a.x] = v[k] * __uint_as_float(a.y);
+      }
+    }
+    group_sync<T>(gid);
+    lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
+    group_sync<T>(gid);
+    // ---- H (second), ending in layout L
+    middle_rounds_then_L<C, 0, R>(s, tid, gid, v);
+    butterflies<R, C::PL, C::PL>(v);
+    // ---- C * scale, feature epilogue
+    const float* csp = p.cs + (int64_t)e * N;
+#pragma unroll
+    for (int j = 0; j < R / 4; ++j) {
+      const int i0 = 4 * (int)tid + j * 4 * T;
+      const float4 c4 = __ldg(reinterpret_cast<const float4*>(csp + i0));
+      float z[4] = {v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]};
+      const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) z[c] = FOLD ? z[c] * cc[c] : (z[c] * cc[c]) * p.scale;
+      if (valid) {
+        float* o = orow + (int64_t)e * N + i0;
+        if constexpr (FEAT) {
+          float sn[4], cn[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sincos_fast(z[c], sn[c], cn[c]);
+            sn[c] *= p.norm;
+            cn[c] *= p.norm;
+          }
+          *reinterpret_cast<float4*>(o) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+          *reinterpret_cast<float4*>(o + p.D) = make_float4(sn[0], sn[1], sn[2], sn[3]);
+        } else {
+          *reinterpret_cast<float4*>(o) = make_float4(z[0], z[1], z[2], z[3]);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- parity variant
+// One CTA per (row, block); follows fastfood.py:189-197 operation by operation.
+__device__ void parity_wht_smem(float* a, float* tmp, int n) {
+  const int base = n < 256 ? n : 256;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int c0 = j - (j % base), jj = j % base;
+    float acc = 0.0f;
+    for (int k = 0; k < base; ++k) {
+      const float xk = a[c0 + k];
+      acc = (__popc((unsigned)(k & jj)) & 1) ? acc - xk : acc + xk;
+    }
+    tmp[j] = acc;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) a[j] = tmp[j];
+  __syncthreads();
+  for (int h = base; h < n; h <<= 1) {
+    for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
+      const int grp = t / h, off = t % h;
+      float* pa = a + grp * 2 * h + off;
+      float* pb = pa + h;
+      const float sum = *pa + *pb;
+      *pa = sum;
+      *pb = sum - 2.0f * *pb;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_fastfood_parity(const float* x, int64_t ldx, int32_t d, const int32_t* rows,
+                                  int64_t n, const float* b, const int32_t* perm, const float* g,
+                                  const float* c, float scale, int feat, float norm, float* out,
+                                  int64_t ldo, int64_t D) {
+  extern __shared__ float pz[];
+  float* a = pz;
+  float* tmp = pz + n;
+  const int64_t row = blockIdx.x;
+  const int e = blockIdx.y;
+  const int64_t src = rows ? (int64_t)rows[row] : row;
+  const float* xp = x + src * ldx;
+  const int64_t off = (int64_t)e * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = (i < d ? xp[i] : 0.0f) * b[off + i];
+  __syncthreads();
+  parity_wht_smem(a, tmp, (int)n);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tmp[i] = a[perm[off + i]];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[i] = tmp[i] * g[off + i];
+  __syncthreads();
+  parity_wht_smem(a, tmp, (int)n);
+  float* o = out + row * ldo + off;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float z = (a[i] * c[off + i]) * scale;
+    if (feat) {
+      o[i] = cosf(z) * norm;
+      o[i + D] = sinf(z) * norm;
+    } else {
+      o[i] = z;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dispatch
+template <class C>
+int prepare_cfg(const TablesView& tv, cudaStream_t st) {
+  const int64_t total = (int64_t)tv.E * C::R * C::T;
+  unsigned grid = (unsigned)((total + 255) / 256);
+  if (grid > 148 * 32) grid = 148 * 32;
+  k_prepare<C><<<grid, 256, 0, st>>>(tv.b, tv.g, tv.perminv, tv.E, tv.bmask, tv.scat);
+  return check_launch("k_prepare");
+}
+
+int ff_logr(int logn);  // below
+
+int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st, bool validate) {
+  const int64_t total = tv.n * tv.E;
+  unsigned grid = (unsigned)((total + 255) / 256);
+  if (grid > 148 * 32) grid = 148 * 32;
+  MCK_TRY(check_cuda(cudaMemsetAsync(tv.flag, 0, 4, st), "flag reset"));
+  k_perminv<<<grid, 256, 0, st>>>(tv.perm, tv.n, tv.E, tv.perminv, tv.flag);
+  MCK_TRY(check_launch("k_perminv"));
+  if (validate) {
+    k_perm_check<<<grid, 256, 0, st>>>(tv.perm, tv.perminv, tv.n, tv.E, tv.flag);
+    MCK_TRY(check_launch("k_perm_check"));
+    int32_t h = 0;
+    MCK_TRY(check_cuda(cudaMemcpyAsync(&h, tv.flag, 4, cudaMemcpyDeviceToHost, st), "flag copy"));
+    MCK_TRY(check_cuda(cudaStreamSynchronize(st), "flag sync"));
+    if (h) return fail_value("permutation is not a bijection on {0..n-1}");
+  }
+  k_cscale<<<grid, 256, 0, st>>>(tv.c, total, scale, fold, tv.cs);
+  MCK_TRY(check_launch("k_cscale"));
+  int logn = 0;
+  while ((int64_t(1) << logn) < tv.n) ++logn;
+  switch (logn) {
+    case 3: return prepare_cfg<RowCfg<3, 2>>(tv, st);
+    case 4: return prepare_cfg<RowCfg<4, 3>>(tv, st);
+    case 5: return prepare_cfg<RowCfg<5, 4>>(tv, st);
+    case 6: return prepare_cfg<RowCfg<6, 4>>(tv, st);
+    case 7: return prepare_cfg<RowCfg<7, 5>>(tv, st);
+    case 8: return prepare_cfg<RowCfg<8, 5>>(tv, st);
+    case 9: return prepare_cfg<RowCfg<9, 5>>(tv, st);
+    case 10: return prepare_cfg<RowCfg<10, 5>>(tv, st);
+    case 11: return prepare_cfg<RowCfg<11, 5>>(tv, st);
+    case 12: return prepare_cfg<RowCfg<12, 5>>(tv, st);
+    case 13: return prepare_cfg<RowCfg<13, 5>>(tv, st);
+    case 14: return prepare_cfg<RowCfg<14, 5>>(tv, st);
+    default: return MCK_OK;  // fused kernel not available; parity path only
+  }
+}
+
+template <class C, bool FEAT, bool FOLD, bool VEC>
+int launch_ff(const FFParams& p, cudaStream_t st) {
+  constexpr int ROWS = ff_rows_per_cta<C>();
+  const size_t smem = (size_t)ROWS * C::SMEM_FLOATS * sizeof(float);
+  auto kern = k_fastfood<C, FEAT, FOLD, VEC>;
+  if (smem > 48 * 1024)
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "fastfood smem"));
+  const int64_t blocks = (p.m + ROWS - 1) / ROWS;
+  FFParams q = p;
+  for (int64_t b0 = 0; b0 < blocks; b0 += (1ll << 30)) {
+    const int64_t nb = blocks - b0 < (1ll << 30) ? blocks - b0 : (1ll << 30);
+    q.m = p.m - b0 * ROWS;
+    q.out = p.out + b0 * ROWS * p.ldo;
+    if (p.rows) q.rows = p.rows + b0 * ROWS;
+    else q.x = p.x + b0 * ROWS * p.ldx;
+    kern<<<(unsigned)nb, C::T * ROWS, smem, st>>>(q);
+  }
+  return check_launch("k_fastfood");
+}
+
+template <class C>
+int launch_ff_cfg(const FFParams& p, bool feat, bool fold, bool vec, cudaStream_t st) {
+  if (feat) {
+    if (fold) return vec ? launch_ff<C, true, true, true>(p, st) : launch_ff<C, true, true, false>(p, st);
+    return vec ? launch_ff<C, true, false, true>(p, st) : launch_ff<C, true, false, false>(p, st);
+  }
+  if (fold) return vec ? launch_ff<C, false, true, true>(p, st) : launch_ff<C, false, true, false>(p, st);
+  return vec ? launch_ff<C, false, false, true>(p, st) : launch_ff<C, false, false, false>(p, st);
+}
+
+int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                 int64_t ldx, const int32_t* rows, bool feat, bool normalize, float* out,
+                 int64_t ldo, int variant, cudaStream_t st) {
+  if (m == 0) return MCK_OK;
+  const int64_t n = tv.n;
+  const int64_t D = n * tv.E;
+  // fastfood.py:186 scale = float32(1/(sigma*sqrt(n))); :225 float32(1/sqrt(D))
+  const double scale_d = 1.0 / (sigma * sqrt((double)n));
+  const float scale = (float)scale_d;
+  const float norm = normalize ? (float)(1.0 / sqrt((double)D)) : 1.0f;
+  int ex = 0;
+  const bool fold = frexpf(scale, &ex) == 0.5f;  // power of two
+  int logn = 0;
+  while ((int64_t(1) << logn) < n) ++logn;
+  if (variant == MCK_WHT_PARITY || logn < 3 || logn > 14) {
+    const size_t smem = (size_t)2 * n * sizeof(float);
+    if (smem > 200 * 1024) return fail_value("parity expansion supports padded_dim <= 16384");
+    if (smem > 48 * 1024)
+      MCK_TRY(check_cuda(cudaFuncSetAttribute(k_fastfood_parity,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem), "parity smem"));
+    if (variant != MCK_WHT_PARITY && logn > 14)
+      return fail_value("padded_dim %lld exceeds the fused kernel's maximum 16384", (long long)n);
+    for (int64_t r0 = 0; r0 < m; r0 += 65535) {
+      const int64_t nr = m - r0 < 65535 ? m - r0 : 65535;
+      dim3 grid((unsigned)nr, (unsigned)tv.E);
+      k_fastfood_parity<<<grid, n < 256 ? (unsigned)((n + 31) / 32 * 32) : 256u, smem, st>>>(
+          rows ? x : x + r0 * ldx, ldx, d, rows ? rows + r0 : nullptr, n, tv.b, tv.perm, tv.g,
+          tv.c, scale, feat ? 1 : 0, norm, out + r0 * ldo, ldo, D);
+      MCK_TRY(check_launch("k_fastfood_parity"));
+    }
+    return MCK_OK;
+  }
+  FFParams p{};
+  p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
+  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs;
+  p.scale = scale; p.norm = norm; p.out = out; p.ldo = ldo; p.E = tv.E; p.D = D;
+  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  if ((ldo % 4) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return fail_value("output rows must be 16-byte aligned");
+  switch (logn) {
+    case 3: return launch_ff_cfg<RowCfg<3, 2>>(p, feat, fold, vec, st);
+    case 4: return launch_ff_cfg<RowCfg<4, 3>>(p, feat, fold, vec, st);
+    case 5: return launch_ff_cfg<RowCfg<5, 4>>(p, feat, fold, vec, st);
+    case 6: return launch_ff_cfg<RowCfg<6, 4>>(p, feat, fold, vec, st);
+    case 7: return launch_ff_cfg<RowCfg<7, 5>>(p, feat, fold, vec, st);
+    case 8: return launch_ff_cfg<RowCfg<8, 5>>(p, feat, fold, vec, st);
+    case 9: return launch_ff_cfg<RowCfg<9, 5>>(p, feat, fold, vec, st);
+    case 10: return launch_ff_cfg<RowCfg<10, 5>>(p, feat, fold, vec, st);
+    case 11: return launch_ff_cfg<RowCfg<11, 5>>(p, feat, fold, vec, st);
+    case 12: return launch_ff_cfg<RowCfg<12, 5>>(p, feat, fold, vec, st);
+    case 13: return launch_ff_cfg<RowCfg<13, 5>>(p, feat, fold, vec, st);
+    case 14: return launch_ff_cfg<RowCfg<14, 5>>(p, feat, fold, vec, st);
+    default: return fail_value("unsupported padded_dim %lld", (long long)n);
+  }
+}
+
+}  // namespace mck

@@ -1,0 +1,262 @@
+// K1 -- batched in-place Walsh-Hadamard transform (replaces wht.py:142-162).
+//
+// fast variant
+//   n <= 2^15 : one thread group per row (fwht_core.cuh), rows stay in
+//               registers; 16-byte coalesced global loads/stores.
+//   n >= 2^16 : the row is viewed as [N1][N2] (N2 = 2^14).  Phase A
+//               transforms the N1-long columns (each thread one column, in
+//               registers); phase B runs the register kernel on the N1
+//               contiguous N2-segments.  Rows are processed in chunks small
+//               enough (<= 24 MiB) that phase B finds phase A's output in the
+//               126 MB L2, so HBM sees about one read and one write.
+// parity variant (verification only; bit-exact to the reference on
+//   OpenBLAS SkylakeX): every aligned base chunk (256) becomes the sequential
+//   fp32 sum over k of H[k][j]*x_k, then combine stages (a+b, (a+b)-2b).
+#include "mck_common.cuh"
+#include "fwht_core.cuh"
+
+namespace mck {
+
+template <class V> struct Vec4;
+template <> struct Vec4<float> {
+  __device__ static void load(const float* p, float (&o)[4]) {
+    float4 t = *reinterpret_cast<const float4*>(p);
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  }
+  __device__ static void store(float* p, const float (&o)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+};
+template <> struct Vec4<double> {
+  __device__ static void load(const double* p, double (&o)[4]) {
+    double2 a = reinterpret_cast<const double2*>(p)[0];
+    double2 b = reinterpret_cast<const double2*>(p)[1];
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+  }
+  __device__ static void store(double* p, const double (&o)[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(o[0], o[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(o[2], o[3]);
+  }
+};
+
+// Load/store a whole row in layout L (register k: index bits {0,1} from k&3,
+// top bits from k>>2; thread id on bits 2..).
+template <class C, class V>
+__device__ __forceinline__ void load_row_L(const V* row, uint32_t tid, V (&v)[C::R]) {
+#pragma unroll
+  for (int j = 0; j < C::R / 4; ++j) {
+    V t[4];
+    Vec4<V>::load(row + 4 * tid + (size_t)j * (4 * C::T), t);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[4 * j + c] = t[c];
+  }
+}
+template <class C, class V>
+__device__ __forceinline__ void store_row_L(V* row, uint32_t tid, const V (&v)[C::R]) {
+#pragma unroll
+  for (int j = 0; j < C::R / 4; ++j) {
+    V t[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) t[c] = v[4 * j + c];
+    Vec4<V>::store(row + 4 * tid + (size_t)j * (4 * C::T), t);
+  }
+}
+
+template <class C>
+constexpr int rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
+
+template <class C, class V>
+__global__ void __launch_bounds__(C::T * rows_per_cta<C>())
+fwht_rows_kernel(V* __restrict__ data, int64_t rows) {
+  constexpr int ROWS = rows_per_cta<C>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* smem = reinterpret_cast<V*>(smem_raw);
+  const int gid = threadIdx.x / C::T;
+  const uint32_t tid = threadIdx.x % C::T;
+  V* s = smem + gid * C::SMEM_FLOATS;
+  const int64_t row = (int64_t)blockIdx.x * ROWS + gid;
+  if (row >= rows) return;  // whole groups exit together
+  V* p = data + row * (int64_t)C::N;
+  V v[C::R];
+  load_row_L<C>(p, tid, v);
+  butterflies<C::R, C::PL, C::PL>(v);
+  middle_rounds<C, 0, C::PL>(s, tid, gid, v);
+  constexpr uint32_t PM = last_mid_regs<C>();
+  sts_layout<C::R, PM>(s, thread_part<C::FULL, PM>(tid), v);
+  group_sync<C::T>(gid);
+  lds_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
+  store_row_L<C>(p, tid, v);
+}
+
+template <class C, class V>
+int launch_rows(V* data, int64_t rows, cudaStream_t st) {
+  constexpr int ROWS = rows_per_cta<C>();
+  const size_t smem = (size_t)ROWS * C::SMEM_FLOATS * sizeof(V);
+  auto kern = fwht_rows_kernel<C, V>;
+  if (smem > 48 * 1024) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "fwht smem attribute"));
+  }
+  const int64_t blocks = (rows + ROWS - 1) / ROWS;
+  for (int64_t b0 = 0; b0 < blocks; b0 += (1ll << 30)) {
+    const int64_t nb = blocks - b0 < (1ll << 30) ? blocks - b0 : (1ll << 30);
+    kern<<<(unsigned)nb, C::T * ROWS, smem, st>>>(data + b0 * ROWS * (int64_t)C::N,
+                                                  rows - b0 * ROWS);
+  }
+  return check_launch("fwht_rows_kernel");
+}
+
+// Phase A of the large-n path: H_{N1} along the column index of the
+// [N1][N2] view, one thread per column, all N1 values in registers.
+template <int LOGN1, class V>
+__global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, int64_t rows,
+                                                        int n2) {
+  constexpr int N1 = 1 << LOGN1;
+  const int64_t col_blocks = n2 / 256;
+  const int64_t row = blockIdx.x / col_blocks;
+  const int64_t col = (blockIdx.x % col_blocks) * 256 + threadIdx.x;
+  if (row >= rows) return;
+  V* p = data + row * (int64_t)N1 * n2 + col;
+  V v[N1];
+#pragma unroll
+  for (int i = 0; i < N1; ++i) v[i] = p[(int64_t)i * n2];
+#pragma unroll
+  for (int h = 1; h < N1; h <<= 1) {
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      if (!(i & h)) {
+        V a = v[i], b = v[i | h];
+        v[i] = a + b;
+        v[i | h] = a - b;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N1; ++i) p[(int64_t)i * n2] = v[i];
+}
+
+template <class V>
+int launch_rows_by_logn(V* data, int64_t rows, int logn, cudaStream_t st) {
+  switch (logn) {
+    case 3: return launch_rows<RowCfg<3, 2>, V>(data, rows, st);
+    case 4: return launch_rows<RowCfg<4, 3>, V>(data, rows, st);
+    case 5: return launch_rows<RowCfg<5, 4>, V>(data, rows, st);
+    case 6: return launch_rows<RowCfg<6, 4>, V>(data, rows, st);
+    case 7: return launch_rows<RowCfg<7, 5>, V>(data, rows, st);
+    case 8: return launch_rows<RowCfg<8, 5>, V>(data, rows, st);
+    case 9: return launch_rows<RowCfg<9, 5>, V>(data, rows, st);
+    case 10: return launch_rows<RowCfg<10, 5>, V>(data, rows, st);
+    case 11: return launch_rows<RowCfg<11, 5>, V>(data, rows, st);
+    case 12: return launch_rows<RowCfg<12, 5>, V>(data, rows, st);
+    case 13: return launch_rows<RowCfg<13, 5>, V>(data, rows, st);
+    case 14: return launch_rows<RowCfg<14, 5>, V>(data, rows, st);
+    case 15:
+      if (sizeof(V) == 4) return launch_rows<RowCfg<15, 5>, V>(data, rows, st);
+      return fail_value("internal: fp64 rows kernel limited to 2^14");
+    default: return fail_value("internal: no row kernel for 2^%d", logn);
+  }
+}
+
+template <class V>
+int launch_cols(V* data, int64_t rows, int logn1, int n2, cudaStream_t st) {
+  const int64_t grid = rows * (n2 / 256);
+  switch (logn1) {
+#define MCK_COLS(L) \
+  case L: fwht_cols_kernel<L, V><<<(unsigned)grid, 256, 0, st>>>(data, rows, n2); break;
+    MCK_COLS(1) MCK_COLS(2) MCK_COLS(3) MCK_COLS(4) MCK_COLS(5) MCK_COLS(6)
+#undef MCK_COLS
+    default: return fail_value("internal: no column kernel for 2^%d", logn1);
+  }
+  return check_launch("fwht_cols_kernel");
+}
+
+// tiny rows: one thread per row, serial butterflies (n <= 4)
+template <class V>
+__global__ void fwht_tiny_kernel(V* data, int64_t rows, int n) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  V* p = data + r * n;
+  for (int h = 1; h < n; h <<= 1)
+    for (int i = 0; i < n; ++i)
+      if (!(i & h)) { V a = p[i], b = p[i | h]; p[i] = a + b; p[i | h] = a - b; }
+}
+
+template <class V>
+int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
+  int logn = 0;
+  while ((int64_t(1) << logn) < n) ++logn;
+  if (rows == 0 || n == 1) return MCK_OK;
+  const int max_row_logn = sizeof(V) == 4 ? 15 : 14;
+  if (logn <= 2) {
+    fwht_tiny_kernel<V><<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(data, rows, (int)n);
+    return check_launch("fwht_tiny_kernel");
+  }
+  if (logn <= max_row_logn) return launch_rows_by_logn<V>(data, rows, logn, st);
+  const int logn2 = 14, logn1 = logn - logn2;
+  if (logn1 > 6) return fail_value("length %lld exceeds the supported maximum 2^20", (long long)n);
+  const int n2 = 1 << logn2;
+  // chunk so that one chunk (<= 24 MiB) stays L2-resident between phases
+  int64_t chunk = (24ll << 20) / (n * (int64_t)sizeof(V));
+  if (chunk < 1) chunk = 1;
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
+    V* p = data + r0 * n;
+    MCK_TRY(launch_cols<V>(p, nr, logn1, n2, st));
+    MCK_TRY(launch_rows_by_logn<V>(p, nr << logn1, logn2, st));
+  }
+  return MCK_OK;
+}
+
+// ---------------------------------------------------------------- parity
+// Base chunks: y_j = sum_{k=0..B-1} H[k][j] x_k accumulated sequentially in
+// fp32 (products by +-1 exact), one thread per output element.
+__global__ void parity_base_kernel(float* __restrict__ data, int64_t chunks, int base) {
+  extern __shared__ float sx[];
+  const int64_t c = blockIdx.x;
+  if (c >= chunks) return;
+  float* p = data + c * base;
+  for (int i = threadIdx.x; i < base; i += blockDim.x) sx[i] = p[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < base; j += blockDim.x) {
+    float acc = 0.0f;
+    for (int k = 0; k < base; ++k) {
+      const float xk = sx[k];
+      acc = (__popc((unsigned)(k & j)) & 1) ? acc - xk : acc + xk;
+    }
+    p[j] = acc;
+  }
+}
+
+// One combine stage at span h: a' = a + b ; b' = a' - 2b  (wht.py:115-126).
+__global__ void parity_combine_kernel(float* __restrict__ data, int64_t total_pairs, int64_t h) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total_pairs) return;
+  const int64_t grp = t / h, off = t % h;
+  float* a = data + grp * 2 * h + off;
+  float* b = a + h;
+  const float s = *a + *b;
+  *a = s;
+  *b = s - 2.0f * *b;
+}
+
+int fwht_parity(float* data, int64_t rows, int64_t n, cudaStream_t st) {
+  if (rows == 0) return MCK_OK;
+  const int base = n < 256 ? (int)n : 256;
+  const int64_t chunks = rows * (n / base);
+  // first element of the base: y_j starts at 0 + (+-x_0); adding to 0.0f is
+  // exact, so this equals the BLAS accumulation order.
+  parity_base_kernel<<<(unsigned)chunks, base < 256 ? base : 256, base * sizeof(float), st>>>(
+      data, chunks, base);
+  MCK_TRY(check_launch("parity_base_kernel"));
+  const int64_t pairs = rows * n / 2;
+  for (int64_t h = base; h < n; h <<= 1) {
+    parity_combine_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, st>>>(data, pairs, h);
+    MCK_TRY(check_launch("parity_combine_kernel"));
+  }
+  return MCK_OK;
+}
+
+template int fwht_fast<float>(float*, int64_t, int64_t, cudaStream_t);
+template int fwht_fast<double>(double*, int64_t, int64_t, cudaStream_t);
+
+}  // namespace mck

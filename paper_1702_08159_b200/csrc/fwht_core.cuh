@@ -1,0 +1,193 @@
+// Register-resident Walsh-Hadamard core for one row of N = 2^LOGN elements
+// held by a group of T = N / R threads (R = 2^LOGR elements per thread).
+//
+// The unnormalised transform is the tensor product of independent 2-point
+// butterflies on every index bit, so stages commute: a thread butterflies
+// whichever LOGR index bits it currently holds in registers ("a round"),
+// then the group exchanges elements through shared memory so that other bits
+// become register-resident.  A row therefore costs one coalesced global read
+// and one global write plus ceil(log2(T)/LOGR) shared-memory exchanges.
+//
+// Layouts (register bit set P; thread-id bits fill the remaining bits in
+// ascending order):
+//   L  : P = {0,1} U top (LOGR-2) bits  -> 16-byte vector global access,
+//        lanes on bits 2..6 (coalesced 512 B per warp instruction)
+//   M_j: P = middle bits 2+j*LOGR ... (plus unused "filler" high bits when
+//        fewer than LOGR middle bits remain)
+// Shared memory uses one pad word per 32 (addr = i + i/32), which makes every
+// layout above bank-conflict free for scalar LDS/STS.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mck {
+
+__host__ __device__ constexpr uint32_t deposit_bits(uint32_t v, uint32_t mask) {
+  uint32_t out = 0;
+  int src = 0;
+  for (int b = 0; b < 32; ++b) {
+    if (mask & (1u << b)) {
+      if (v & (1u << src)) out |= 1u << b;
+      ++src;
+    }
+  }
+  return out;
+}
+
+__host__ __device__ constexpr int popcount_c(uint32_t m) {
+  int c = 0;
+  for (int b = 0; b < 32; ++b) c += (m >> b) & 1u;
+  return c;
+}
+
+__host__ __device__ __forceinline__ constexpr uint32_t pad_addr(uint32_t i) { return i + (i >> 5); }
+
+template <int LOGN_, int LOGR_>
+struct RowCfg {
+  static constexpr int LOGN = LOGN_;
+  static constexpr int LOGR = LOGR_;
+  static constexpr int N = 1 << LOGN;
+  static constexpr int R = 1 << LOGR;
+  static constexpr int LOGT = LOGN - LOGR;
+  static constexpr int T = 1 << LOGT;
+  static constexpr uint32_t FULL = (uint32_t)N - 1u;
+  static_assert(LOGR >= 2 && LOGN >= LOGR + 1, "row config");
+  // layout L
+  static constexpr uint32_t PL =
+      3u | ((((1u << (LOGR - 2)) - 1u)) << (LOGN - LOGR + 2));
+  // middle bits 2 .. 2+LOGT-1
+  static constexpr int NMID = (LOGT + LOGR - 1) / LOGR;
+  static constexpr int SMEM_FLOATS = N + N / 32;  // padded row
+
+  // Active (butterflied) middle bits of round j.
+  __host__ __device__ static constexpr uint32_t mid_active(int j) {
+    int lo = 2 + j * LOGR;
+    int hi = lo + LOGR;
+    if (hi > 2 + LOGT) hi = 2 + LOGT;
+    uint32_t m = 0;
+    for (int b = lo; b < hi; ++b) m |= 1u << b;
+    return m;
+  }
+  // Register bits of middle round j: active bits plus fillers taken from the
+  // top of the index (never middle bits), so that every round holds R values.
+  __host__ __device__ static constexpr uint32_t mid_regs(int j) {
+    uint32_t m = mid_active(j);
+    int need = LOGR - popcount_c(m);
+    for (int b = LOGN - 1; need > 0 && b >= 0; --b) {
+      if (!(m & (1u << b)) && !(mid_active_all() & (1u << b))) {
+        m |= 1u << b;
+        --need;
+      }
+    }
+    return m;
+  }
+  __host__ __device__ static constexpr uint32_t mid_active_all() {
+    uint32_t m = 0;
+    for (int b = 2; b < 2 + LOGT; ++b) m |= 1u << b;
+    return m;
+  }
+};
+
+// Element index of register k in a layout with register mask P, for a thread
+// whose thread-bit contribution is `tpart` (= deposit(tid, ~P)).
+template <uint32_t P>
+__device__ __forceinline__ uint32_t lay_index(uint32_t tpart, int k) {
+  return tpart | deposit_bits((uint32_t)k, P);
+}
+
+template <uint32_t FULL, uint32_t P>
+__device__ __forceinline__ uint32_t thread_part(uint32_t tid) {
+  return deposit_bits(tid, FULL & ~P);
+}
+
+// Butterflies over the register-index bits whose deposited index bit is in
+// ACTIVE (a subset of P).
+template <int R, uint32_t P, uint32_t ACTIVE, class V>
+__device__ __forceinline__ void butterflies(V (&v)[R]) {
+#pragma unroll
+  for (int a = 0; (1 << a) < R; ++a) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    if (ACTIVE & deposit_bits(1u << a, P)) {
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (!(k & (1 << a))) {
+          V x = v[k], y = v[k | (1 << a)];
+          v[k] = x + y;
+          v[k | (1 << a)] = x - y;
+        }
+      }
+    }
+  }
+}
+
+template <int R, uint32_t P, class V>
+__device__ __forceinline__ void sts_layout(V* s, uint32_t tpart, const V (&v)[R]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) s[pad_addr(lay_index<P>(tpart, k))] = v[k];
+}
+
+template <int R, uint32_t P, class V>
+__device__ __forceinline__ void lds_layout(const V* s, uint32_t tpart, V (&v)[R]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = s[pad_addr(lay_index<P>(tpart, k))];
+}
+
+// Group barrier for T threads that start at a multiple of T inside the CTA.
+template <int T>
+__device__ __forceinline__ void group_sync(int group_id) {
+  if constexpr (T <= 32) {
+    __syncwarp();
+  } else {
+    // named barrier per group (ids 1..15); T threads participate
+    asm volatile("bar.sync %0, %1;" ::"r"(group_id + 1), "r"(T) : "memory");
+  }
+}
+
+// Middle rounds, compile-time recursion over j: exchange from layout PREV
+// into round j, butterfly its active bits.
+template <class C, int J, uint32_t PREV, int R, class V>
+__device__ __forceinline__ void middle_rounds(V* s, uint32_t tid, int gid, V (&v)[R]) {
+  if constexpr (J < C::NMID) {
+    constexpr uint32_t PJ = C::mid_regs(J);
+    constexpr uint32_t AJ = C::mid_active(J);
+    sts_layout<R, PREV>(s, thread_part<C::FULL, PREV>(tid), v);
+    group_sync<C::T>(gid);
+    lds_layout<R, PJ>(s, thread_part<C::FULL, PJ>(tid), v);
+    group_sync<C::T>(gid);
+    butterflies<R, PJ, AJ>(v);
+    middle_rounds<C, J + 1, PJ, R>(s, tid, gid, v);
+  }
+}
+
+// Register mask of the last middle round (the layout the row is in after
+// middle_rounds<C, 0, ...>).
+template <class C>
+__host__ __device__ constexpr uint32_t last_mid_regs() {
+  return C::mid_regs(C::NMID - 1);
+}
+
+// Reverse order for the second transform of the Fastfood block: middle
+// rounds first (starting from data already laid out in round 0's registers),
+// finishing with an exchange back to layout L.
+template <class C, int J, int R, class V>
+__device__ __forceinline__ void middle_rounds_then_L(V* s, uint32_t tid, int gid, V (&v)[R]) {
+  constexpr uint32_t PJ = C::mid_regs(J);
+  butterflies<R, PJ, C::mid_active(J)>(v);
+  if constexpr (J + 1 < C::NMID) {
+    constexpr uint32_t PN = C::mid_regs(J + 1);
+    sts_layout<R, PJ>(s, thread_part<C::FULL, PJ>(tid), v);
+    group_sync<C::T>(gid);
+    lds_layout<R, PN>(s, thread_part<C::FULL, PN>(tid), v);
+    group_sync<C::T>(gid);
+    middle_rounds_then_L<C, J + 1, R>(s, tid, gid, v);
+  } else {
+    sts_layout<R, PJ>(s, thread_part<C::FULL, PJ>(tid), v);
+    group_sync<C::T>(gid);
+    lds_layout<R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
+    group_sync<C::T>(gid);
+  }
+}
+
+}  // namespace mck

@@ -1,0 +1,388 @@
+"""GPU parity: the CUDA library (through the C ABI) against the reference's
+golden vectors and the CPU oracle, on the same seeded inputs.
+
+Tolerances (written per test):
+* integer / index work (hashes, uniforms, signs, permutations, B): bit-exact;
+* float64-derived factors G, C: bit-exact expected; the mismatch count is
+  asserted to be 0 and reported;
+* transforms: scale-relative 1e-6 against the float64 oracle (the reference's
+  own criterion, pkg/tests/test_acceptance.py:50-63); the parity variant is
+  bit-exact against the reference;
+* features: normalised features within rtol 1e-5 / atol 1e-6 (north star);
+  z within 2e-6 * max|z|.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import load_json, load_npz
+from oracle import detrand as od
+from oracle import fastfood as off
+from oracle import linear_model as olm
+from oracle import wht as ow
+from paper_1702_08159_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def _spec(c):
+    import paper_1702_08159_b200 as P
+    k = P.RBF(c["sigma"]) if c["kind"] == "rbf" else P.RBFMatern(c["sigma"], c["t"])
+    return P.FeatureMapSpec(c["d"], c["E"], k, c["seed"])
+
+
+# ---------------------------------------------------------------- randomness
+class TestStreams:
+    def test_streams_bit_exact(self, cuda):
+        from paper_1702_08159_b200.detrand import RandomStream
+        z = load_npz("detrand.npz")
+        cases = json.loads(str(z["cases"][0]))
+        for k, (seed, label, block) in enumerate(cases):
+            h = RandomStream(seed, label, block).hashes(64).cpu().numpy().view(np.uint64)
+            np.testing.assert_array_equal(h, z[f"hash{k}"])
+            u = RandomStream(seed, label, block).uniform01_array(64).cpu().numpy()
+            np.testing.assert_array_equal(u, z[f"uni{k}"])
+            s = RandomStream(seed, label, block).sign_array(64).cpu().numpy()
+            np.testing.assert_array_equal(s, z[f"sign{k}"])
+            st = RandomStream(seed, label, block)
+            g = np.concatenate([st.gaussian_array(5).cpu().numpy(),
+                                st.gaussian_array(60).cpu().numpy()])
+            np.testing.assert_allclose(g, z[f"gauss{k}"], rtol=1e-12, atol=0)
+            assert st.counter == int(z[f"gauss_counter{k}"][0])
+
+    def test_reference_golden_constants(self, cuda):
+        from paper_1702_08159_b200.detrand import RandomStream
+        assert RandomStream(42, "B", 0).hash64() == 0x1E33DE85387EAE97
+        assert RandomStream(42, "G", 0).hash64() == 0xCE29D5FF2B3CD5DA
+        assert RandomStream(43, "B", 0).hash64() == 0xD3E8DB5D9D65A34D
+        assert RandomStream(7, "u").uniform01_array(4).tolist() == [
+            0.19681970807755012, 0.3875403325733868, 0.9742781761190904, 0.6916958472993927]
+        np.testing.assert_allclose(RandomStream(7, "g").gaussian_array(4).cpu().numpy(),
+                                   [0.1577956022387008, -1.074844538017888,
+                                    0.5536515769773818, -0.3044021609698588], rtol=1e-12)
+        assert RandomStream(7, "s").sign_array(6).tolist() == [-1, 1, -1, -1, 1, 1]
+
+    def test_permutations_bit_exact(self, cuda):
+        from paper_1702_08159_b200.detrand import fisher_yates_permutations
+        z = load_npz("detrand.npz")
+        assert fisher_yates_permutations(42, "Pi", 0, 1, 4)[0].tolist() == [2, 0, 3, 1]
+        np.testing.assert_array_equal(fisher_yates_permutations(3, "Pi", 1, 1, 1000)[0].cpu().numpy(),
+                                      z["perm_n1000_s3"])
+        got = fisher_yates_permutations(0, "shuffle", 0, 2, 60000).cpu().numpy()
+        np.testing.assert_array_equal(got[0], z["shuffle60000_e0"])
+        np.testing.assert_array_equal(got[1], z["shuffle60000_e1"])
+        # n > 65536 takes the global-memory path
+        big = fisher_yates_permutations(5, "Pi", 0, 1, 70000)[0].cpu().numpy()
+        np.testing.assert_array_equal(big, od.fisher_yates(od.Stream(5, "Pi", 0), 70000))
+
+
+# ---------------------------------------------------------------- factors
+def _device_blocks(spec):
+    import paper_1702_08159_b200 as P
+    bs = P.build_blocks(spec)
+    return bs, dict(b=bs.b_signs.cpu().numpy(), perm=bs.permutation.cpu().numpy(),
+                    g=bs.g_diag.cpu().numpy(), c=bs.c_diag.cpu().numpy())
+
+
+def _assert_factors(got, want, name):
+    np.testing.assert_array_equal(got["b"], want["b"].astype(np.float32), err_msg=f"{name} B")
+    np.testing.assert_array_equal(got["perm"], want["perm"], err_msg=f"{name} Pi")
+    gm = int((got["g"] != want["g"]).sum())
+    cm = int((got["c"] != want["c"]).sum())
+    print(f"{name}: G mismatches {gm}/{got['g'].size}, C mismatches {cm}/{got['c'].size}")
+    np.testing.assert_allclose(got["g"], want["g"], rtol=2e-7, atol=0)
+    np.testing.assert_allclose(got["c"], want["c"], rtol=2e-7, atol=0)
+    assert gm == 0 and cm == 0, f"{name}: float64-derived factors differ after the fp32 cast"
+
+
+class TestFactors:
+    @pytest.mark.parametrize("name", ["rbf_d4", "matern_d13", "rbf_d1", "matern_d1", "rbf_d100",
+                                      "rbf_d1000", "matern_d700", "matern_d2048"])
+    def test_small_specs(self, cuda, name):
+        z = load_npz("blocks_small.npz")
+        c = json.loads(str(z[f"{name}.spec"][0]))
+        _, got = _device_blocks(_spec(c))
+        _assert_factors(got, {k: z[f"{name}.{k}"] for k in ("b", "perm", "g", "c")}, name)
+
+    @pytest.mark.parametrize("cfg", ["c0", "c2"])
+    def test_config_factors(self, cuda, cfg):
+        z = load_npz(f"{cfg}.npz")
+        meta = json.loads(str(z["meta"][0]))
+        _, got = _device_blocks(_spec(meta))
+        _assert_factors(got, z, cfg)
+
+    def test_config4_factors(self, cuda):
+        z = load_npz("c4_blocks.npz")
+        meta = json.loads(str(z["meta"][0]))
+        _, got = _device_blocks(_spec(meta))
+        for e in (0, 31):
+            want = {"b": z[f"b{e}"], "perm": z[f"perm{e}"], "g": z[f"g{e}"], "c": z[f"c{e}"]}
+            _assert_factors({k: v[e] for k, v in got.items()}, want, f"c4 block {e}")
+
+
+# ---------------------------------------------------------------- transforms
+def _scale_close(got, want, rtol=1e-6):
+    scale = max(float(np.abs(want).max()), 1e-30)
+    np.testing.assert_allclose(got, want, rtol=rtol, atol=rtol * scale)
+
+
+class TestWht:
+    def test_fast_vs_naive_all_sizes(self, cuda):
+        # pkg/tests/test_acceptance.py:50-63: 2^0..2^14, 100 vectors, 1e-6 scale-relative
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        rng = np.random.default_rng(1234)
+        for k in range(0, 15):
+            n = 1 << k
+            x = (rng.standard_normal((100, n)) * rng.uniform(0.5, 2.0)).astype(np.float32)
+            want = ow.wht_naive(x.T.astype(np.float64)).T
+            got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+            _scale_close(got, want)
+
+    def test_large_sizes_vs_reference(self, cuda):
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        z = load_npz("wht.npz")
+        for k in (15, 16, 18, 20):
+            x = synthetic.gaussian_rows(1, 1 << k, seed=100 + k)
+            y = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy()
+            scale = np.abs(z[f"n{k}.head"]).max()
+            np.testing.assert_allclose(y[0, :2048], z[f"n{k}.head"], rtol=1e-5, atol=1e-6 * scale)
+            np.testing.assert_allclose(y[0, -2048:], z[f"n{k}.tail"], rtol=1e-5, atol=1e-6 * scale)
+            ss = float((y.astype(np.float64) ** 2).sum())
+            assert abs(ss - float(z[f"n{k}.sumsq"][0])) <= 1e-5 * ss
+
+    def test_parity_variant_bit_exact(self, cuda):
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        z = load_npz("wht.npz")
+        for k in range(1, 15):
+            x = synthetic.gaussian_rows(3, 1 << k, seed=100 + k)
+            got = wht_fast_batch(torch.from_numpy(x).cuda(), variant="parity").cpu().numpy()
+            np.testing.assert_array_equal(got, z[f"n{k}"], err_msg=f"n=2^{k}")
+        for k in (16, 20):
+            x = synthetic.gaussian_rows(1, 1 << k, seed=100 + k)
+            got = wht_fast_batch(torch.from_numpy(x).cuda(), variant="parity").cpu().numpy()
+            np.testing.assert_array_equal(got[0, :2048], z[f"n{k}.head"])
+            np.testing.assert_array_equal(got[0, -2048:], z[f"n{k}.tail"])
+
+    def test_full_size_properties(self, cuda):
+        # config 1: 2^28 floats per length; involution H(Hx) = n x and Parseval
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        g = torch.Generator(device="cuda").manual_seed(7)
+        for k in (10, 14, 16, 20):
+            n = 1 << k
+            x = torch.randn((1 << 28) // n, n, generator=g, device="cuda")
+            y = wht_fast_batch(x.clone())
+            e_x = (x.double() ** 2).sum(dim=1)
+            e_y = (y.double() ** 2).sum(dim=1)
+            assert torch.allclose(e_y, n * e_x, rtol=1e-5)
+            back = wht_fast_batch(y)
+            err = (back.double() / n - x.double()).abs().max().item()
+            assert err <= 1e-5 * x.abs().max().item() * 64, (k, err)
+            del x, y, back
+
+    def test_float64_and_numpy_in_place(self, cuda):
+        from paper_1702_08159_b200 import wht_fast, wht_fast_batch
+        rng = np.random.default_rng(6)
+        v = rng.standard_normal(512)
+        np.testing.assert_allclose(wht_fast(v.copy()), ow.wht_naive(v), rtol=1e-10, atol=1e-10)
+        m = rng.standard_normal((3, 1 << 16))
+        out = wht_fast_batch(m.copy())
+        np.testing.assert_allclose(out, ow.wht_butterfly_f64(m), rtol=1e-9, atol=1e-9)
+        a = np.array([1.0, 2.0, 3.0, 4.0], dtype=np.float32)
+        assert wht_fast(a) is a and a.tolist() == [10.0, -2.0, -4.0, 0.0]
+        empty = np.zeros((0, 64), dtype=np.float32)
+        assert wht_fast_batch(empty) is empty
+
+
+# ---------------------------------------------------------------- feature map
+class TestFeatures:
+    def _config(self, cfg):
+        import paper_1702_08159_b200 as P
+        z = load_npz(f"{cfg}.npz")
+        meta = json.loads(str(z["meta"][0]))
+        spec = _spec(meta)
+        x = synthetic.image_rows(meta["m"], meta["d"], meta["xseed"])[z["rows"]]
+        return P, z, spec, x
+
+    @pytest.mark.parametrize("cfg", ["c0", "c2"])
+    def test_features_within_tolerance(self, cuda, cfg):
+        P, z, spec, x = self._config(cfg)
+        blocks = P.build_blocks(spec)
+        zz = P.apply_zhat_batch(spec, blocks, x)
+        assert zz.dtype == np.float32 and zz.shape == z["z"].shape
+        scale = float(np.abs(z["z"]).max())
+        dz = float(np.abs(zz - z["z"]).max())
+        print(f"{cfg}: max|dz| = {dz:.3e} ({dz / scale:.2e} of max|z|)")
+        assert dz <= 2e-6 * scale
+        feat = P.feature_map_batch(spec, blocks, x)
+        np.testing.assert_allclose(feat[:, z["feat_cols"]], z["feat"], rtol=1e-5, atol=1e-6)
+        raw = P.feature_map_batch(spec, blocks, x[:2], normalize=False)
+        assert np.abs(raw - z["raw"]).max() <= 1e-4
+
+    def test_parity_variant_z_bit_exact(self, cuda):
+        P, z, spec, x = self._config("c0")
+        zz = P.apply_zhat_batch(spec, P.build_blocks(spec), x, variant="parity")
+        np.testing.assert_array_equal(zz, z["z"])
+
+    @pytest.mark.parametrize("name", ["rbf_d4", "matern_d13", "rbf_d1", "rbf_d100", "rbf_d1000",
+                                      "matern_d700", "matern_d2048"])
+    def test_small_specs(self, cuda, name):
+        import paper_1702_08159_b200 as P
+        zf = load_npz("blocks_small.npz")
+        c = json.loads(str(zf[f"{name}.spec"][0]))
+        spec = _spec(c)
+        x = np.random.default_rng(c["seed"]).standard_normal((5, c["d"])).astype(np.float32)
+        blocks = P.build_blocks(spec)
+        zz = P.apply_zhat_batch(spec, blocks, x)
+        want = zf[f"{name}.z"]
+        zscale = max(np.abs(want).max(), 1e-30)
+        assert np.abs(zz - want).max() <= 2e-6 * zscale
+        # N(0,1) inputs give |z| up to ~100 here, where the reference's own fp32
+        # z error (~1e-6 relative) exceeds 1e-6 absolute after cos/sin; the
+        # feature bound therefore carries the z bound through: 2e-6*max|z|/sqrt(D).
+        dim = spec.padded_dim * spec.expansions
+        np.testing.assert_allclose(P.feature_map_batch(spec, blocks, x), zf[f"{name}.feat"],
+                                   rtol=1e-5, atol=max(1e-6, 2e-6 * zscale / np.sqrt(dim)))
+        zp = P.apply_zhat_batch(spec, blocks, x, variant="parity")
+        if c["d"] > 1:
+            np.testing.assert_array_equal(zp, want)
+
+    def test_dense_oracle_small_n(self, cuda):
+        import paper_1702_08159_b200 as P
+        for d in (3, 8, 13, 16):
+            spec = P.FeatureMapSpec(d, 3, P.RBF(0.9), 77)
+            blocks = P.build_blocks(spec)
+            x = np.random.default_rng(d).standard_normal((4, d)).astype(np.float32)
+            zz = P.apply_zhat_batch(spec, blocks, x)
+            ospec = off.OSpec.of(spec)
+            for e in range(3):
+                b, p, g, c = blocks[e].numpy()
+                blk = off.OBlock(b, p, g, c, e)
+                xp = np.zeros((4, spec.padded_dim)); xp[:, :d] = x
+                want = xp @ off.dense_zhat(ospec, blk).T
+                n = spec.padded_dim
+                np.testing.assert_allclose(zz[:, e * n:(e + 1) * n], want, rtol=1e-5, atol=1e-5)
+
+    def test_gather_stride_and_edge_cases(self, cuda):
+        import paper_1702_08159_b200 as P
+        torch = cuda
+        spec = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3)
+        blocks = P.build_blocks(spec)
+        x = synthetic.image_rows(64, 784, 5)
+        xd = torch.from_numpy(x).cuda()
+        full = P.feature_map_batch(spec, blocks, xd)
+        rows = torch.tensor([5, 0, 63, 5, 17], dtype=torch.int32, device="cuda")
+        out = torch.empty((5, 2 * 1024 * 4), device="cuda")
+        P.feature_map_batch(spec, blocks, xd, out=out, rows=rows)
+        assert torch.equal(out, full[rows.long()])
+        # strided input rows (ldx > d) and a non-multiple-of-4 dimension
+        wide = torch.zeros((64, 800), device="cuda")
+        wide[:, :784] = xd
+        assert torch.equal(P.feature_map_batch(spec, blocks, wide[:, :784]), full)
+        spec2 = P.FeatureMapSpec(783, 2, P.RBF(1.0), 3)
+        b2 = P.build_blocks(spec2)
+        f2 = P.apply_zhat_batch(spec2, b2, x[:, :783])
+        o2 = off.apply_zhat_batch(off.OSpec.of(spec2), [off.OBlock(*b2[e].numpy(), e) for e in range(2)],
+                                  x[:, :783])
+        assert np.abs(f2 - o2).max() <= 2e-6 * np.abs(o2).max()
+        # zero input: cos = 1/sqrt(D), sin = 0
+        zf = P.feature_map_batch(spec, blocks, np.zeros((2, 784), np.float32))
+        assert np.allclose(zf[:, :4096], 1 / 64.0) and np.all(zf[:, 4096:] == 0)
+        # empty batch
+        assert P.feature_map_batch(spec, blocks, np.zeros((0, 784), np.float32)).shape == (0, 8192)
+        with pytest.raises(ValueError, match="features"):
+            P.feature_map_batch(spec, blocks, np.zeros((2, 5), np.float32))
+        with pytest.raises(ValueError, match="blocks"):
+            P.feature_map_batch(spec, list(blocks)[:2], x)
+
+    def test_reference_blocks_upload(self, cuda):
+        import paper_1702_08159_b200 as P
+        z = load_npz("c0.npz")
+        meta = json.loads(str(z["meta"][0]))
+        spec = _spec(meta)
+        ref_blocks = [off.OBlock(z["b"][e].astype(np.float32), z["perm"][e].astype(np.int64),
+                                 z["g"][e], z["c"][e], e) for e in range(meta["E"])]
+        bs = P.blocks_from_reference(spec, ref_blocks)
+        x = synthetic.image_rows(meta["m"], meta["d"], meta["xseed"])[z["rows"]]
+        zz = P.apply_zhat_batch(spec, bs, x, variant="parity")
+        np.testing.assert_array_equal(zz, z["z"])
+
+    def test_unit_norm_and_kernel_estimate(self, cuda):
+        # pkg/tests/test_fastfood.py:232-274: |phi|^2 = 1; mean kernel error
+        # <= 0.05 at d=64, D=512; unbiased over 50 seeds.
+        import paper_1702_08159_b200 as P
+        rng = np.random.default_rng(0)
+        spec = P.FeatureMapSpec(8, 3, P.RBF(1.0), 5)
+        f = P.feature_map_batch(spec, P.build_blocks(spec),
+                                rng.standard_normal((10, 8)).astype(np.float32)).astype(np.float64)
+        np.testing.assert_allclose((f * f).sum(axis=1), 1.0, atol=1e-5)
+
+        def k_exact(a, b, s):
+            return np.exp(-((a.astype(np.float64) - b) ** 2).sum(-1) / (2 * s * s))
+
+        spec = P.FeatureMapSpec(64, 8, P.RBF(1.0), 31)
+        rng = np.random.default_rng(7)
+        x = (rng.standard_normal((100, 64)) * 0.3).astype(np.float32)
+        y = (rng.standard_normal((100, 64)) * 0.3).astype(np.float32)
+        bs = P.build_blocks(spec)
+        est = (P.feature_map_batch(spec, bs, x).astype(np.float64)
+               * P.feature_map_batch(spec, bs, y)).sum(1)
+        assert np.mean(np.abs(est - k_exact(x, y, 1.0))) <= 0.05
+        rng = np.random.default_rng(11)
+        x = (rng.standard_normal(16) * 0.5).astype(np.float32)
+        y = (rng.standard_normal(16) * 0.5).astype(np.float32)
+        ests = []
+        for seed in range(50):
+            spec = P.FeatureMapSpec(16, 4, P.RBF(1.0), seed)
+            bs = P.build_blocks(spec)
+            ests.append(float(np.dot(P.feature_map(spec, bs, x).astype(np.float64),
+                                     P.feature_map(spec, bs, y))))
+        ests = np.array(ests)
+        assert abs(ests.mean() - k_exact(x, y, 1.0)) < 3 * ests.std(ddof=1) / np.sqrt(50) + 1e-4
+
+
+# ---------------------------------------------------------------- softmax head / training
+class TestHead:
+    def test_forward_gradients_vs_oracle(self, cuda):
+        import paper_1702_08159_b200 as P
+        rng = np.random.default_rng(4)
+        x = rng.standard_normal((300, 700)).astype(np.float32)
+        y = rng.integers(0, 10, 300)
+        w = rng.standard_normal((10, 700)) * 0.05
+        b = rng.standard_normal(10) * 0.1
+        model = P.SoftmaxModel(w, b)
+        np.testing.assert_allclose(P.forward_batch(model, x).cpu().numpy(),
+                                   olm.forward_batch(w, b, x), rtol=1e-10, atol=1e-13)
+        assert abs(P.loss(model, x, y, 0.01) - olm.loss(w, b, x, y, 0.01)) <= 1e-10
+        dw, db = P.gradients(model, x, y, 0.01)
+        rdw, rdb = olm.gradients(w, b, x, y, 0.01)
+        np.testing.assert_allclose(dw.cpu().numpy(), rdw, rtol=1e-9, atol=1e-13)
+        np.testing.assert_allclose(db.cpu().numpy(), rdb, rtol=1e-9, atol=1e-13)
+        P.sgd_step(model, x, y, P.TrainConfig(0.5, 300, 1, l2_lambda=0.01))
+        olm.sgd_step(w, b, x, y, 0.5, 0.01)
+        np.testing.assert_allclose(model.w.cpu().numpy(), w, rtol=1e-9, atol=1e-13)
+
+    @pytest.mark.parametrize("golden", ["train_tiny.json", "train_c3h.json", "train_c3.json"])
+    def test_training_matches_reference(self, cuda, golden):
+        import paper_1702_08159_b200 as P
+        g = load_json(golden)
+        c = g["config"]
+        tss = c.get("train_sample_seed")
+        x, y = synthetic.class_images(c["m"], c["d"], 10, seed=c["data_seed"], sample_seed=tss,
+                                      noise=c["noise"])
+        xt, yt = synthetic.class_images(c["m_test"], c["d"], 10, seed=c["data_seed"],
+                                        sample_seed=c["test_sample_seed"], noise=c["noise"])
+        spec = P.FeatureMapSpec(c["d"], c["E"], P.RBF(c["sigma"]), c["seed"])
+        cfg = P.TrainConfig(c["lr"], c["batch"], c["epochs"], shuffle_seed=c["shuffle_seed"])
+        model, met = P.train(spec, P.Dataset(x, y, 10), P.Dataset(xt, yt, 10), cfg)
+        for rec, (e, loss, acc) in zip(met.records, g["history"]):
+            print(f"{golden} epoch {e}: loss {rec.train_loss:.10f} vs {loss:.10f}, "
+                  f"acc {rec.test_acc:.4f} vs {acc:.4f}")
+            assert abs(rec.test_acc - acc) <= 0.002          # 0.2 percentage points
+            assert abs(rec.train_loss - loss) <= 1e-4 * abs(loss) + 1e-7
+        np.testing.assert_allclose(model.b.cpu().numpy(), g["b"], rtol=1e-3, atol=1e-6)
