@@ -21,11 +21,26 @@
 #include "mck_common.cuh"
 #include "fwht_core.cuh"
 #include "tables.cuh"
+#include "async_copy.cuh"
 
 namespace mck {
 
 template <class C>
 constexpr int ff_rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
+
+// Per-block factor tables, staged into shared memory by TMA bulk copies:
+// scat [R][T] uint2 | cs [N] f32 | bmask [bm_stride] u32.
+template <class C>
+constexpr int bm_stride() { return ((((C::R + 31) / 32) * C::T) + 3) & ~3; }
+template <class C>
+constexpr int tab_bytes() { return C::N * 8 + C::N * 4 + bm_stride<C>() * 4; }
+template <class C>
+constexpr int tab_slot() { return (tab_bytes<C>() + 127) & ~127; }
+template <class C>
+constexpr size_t ff_smem_bytes() {
+  return 128 + 2 * (size_t)tab_slot<C>() + (size_t)ff_rows_per_cta<C>() * C::SMEM_FLOATS * 4;
+}
+
 
 // ---------------------------------------------------------------- derived tables
 __global__ void k_perminv(const int32_t* perm, int64_t n, int32_t E, int32_t* perminv,
@@ -82,7 +97,7 @@ __global__ void k_prepare(const float* b, const float* g, const int32_t* perminv
         const uint32_t i = lay_index<C::PL>(thread_part<C::FULL, C::PL>(tid), 32 * k + q);
         if (b[off + i] < 0.0f) bits |= 1u << q;
       }
-      bmask[(e * W + k) * T + tid] = bits;
+      bmask[e * bm_stride<C>() + k * T + tid] = bits;
     }
   }
 }
@@ -112,91 +127,125 @@ struct FFParams {
   int64_t D;
 };
 
+// Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
+// tables of iteration it+1 (next block, or block 0 of the next group) are in
+// flight while iteration it computes.
 template <class C, bool FEAT, bool FOLD, bool VEC>
 __global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>())
 k_fastfood(FFParams p) {
   constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
   constexpr int ROWS = ff_rows_per_cta<C>();
-  extern __shared__ __align__(16) float ff_smem[];
+  constexpr int SLOT = tab_slot<C>();
+  extern __shared__ __align__(128) unsigned char ff_smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ff_smem);
+  unsigned char* tabs = ff_smem + 128;
   const int gid = threadIdx.x / T;
   const uint32_t tid = threadIdx.x % T;
-  float* s = ff_smem + gid * C::SMEM_FLOATS;
-  const int64_t row = (int64_t)blockIdx.x * ROWS + gid;
-  const bool valid = row < p.m;
+  float* s = reinterpret_cast<float*>(ff_smem + 128 + 2 * SLOT) + gid * C::SMEM_FLOATS;
+  constexpr uint32_t P0 = C::mid_regs(0);
 
-  // ---- input row, layout L, zero padded
-  float xr[R];
-  {
-    const int64_t src = valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0;
-    const float* xp = p.x + src * p.ldx;
+  const int64_t groups = (p.m + ROWS - 1) / ROWS;
+  const int64_t my_groups = groups > blockIdx.x ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total_it = my_groups * p.E;
+
+  auto issue = [&](int64_t it) {  // thread 0 only
+    const int e = (int)(it % p.E);
+    unsigned char* dst = tabs + (it & 1) * SLOT;
+    uint64_t* b = bar + (it & 1);
+    mbar_expect_tx(b, tab_bytes<C>());
+    bulk_g2s(dst, p.scat + (int64_t)e * N, N * 8, b);
+    bulk_g2s(dst + N * 8, p.cs + (int64_t)e * N, N * 4, b);
+    bulk_g2s(dst + N * 12, p.bmask + (int64_t)e * bm_stride<C>(), bm_stride<C>() * 4, b);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && total_it > 0) issue(0);
+
+  for (int64_t gi = 0; gi < my_groups; ++gi) {
+    const int64_t row = (blockIdx.x + gi * gridDim.x) * ROWS + gid;
+    const bool valid = row < p.m;
+    // ---- input row, layout L, zero padded (kept in registers for all E blocks)
+    float xr[R];
+    {
+      const int64_t src = valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0;
+      const float* xp = p.x + src * p.ldx;
 #pragma unroll
-    for (int j = 0; j < R / 4; ++j) {
-      const int i0 = 4 * (int)tid + j * 4 * T;
-      if constexpr (VEC) {
-        float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && i0 < p.d) t4 = __ldg(reinterpret_cast<const float4*>(xp + i0));
-        xr[4 * j] = t4.x; xr[4 * j + 1] = t4.y; xr[4 * j + 2] = t4.z; xr[4 * j + 3] = t4.w;
-      } else {
+      for (int j = 0; j < R / 4; ++j) {
+        const int i0 = 4 * (int)tid + j * 4 * T;
+        if constexpr (VEC) {
+          float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid && i0 < p.d) t4 = __ldg(reinterpret_cast<const float4*>(xp + i0));
+          xr[4 * j] = t4.x; xr[4 * j + 1] = t4.y; xr[4 * j + 2] = t4.z; xr[4 * j + 3] = t4.w;
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) xr[4 * j + c] = (valid && i0 + c < p.d) ? __ldg(xp + i0 + c) : 0.f;
+          for (int c = 0; c < 4; ++c) xr[4 * j + c] = (valid && i0 + c < p.d) ? __ldg(xp + i0 + c) : 0.f;
+        }
       }
     }
-  }
-  constexpr uint32_t P0 = C::mid_regs(0);
-  float* orow = p.out + (valid ? row : 0) * p.ldo;
+    float* orow = p.out + (valid ? row : 0) * p.ldo;
 
-  for (int e = 0; e < p.E; ++e) {
-    float v[R];
-    // ---- x * B (sign XOR, exact)
+    for (int e = 0; e < p.E; ++e) {
+      const int64_t it = gi * p.E + e;
+      __syncthreads();  // buffer (it+1)&1 (read at it-1) is free
+      if (threadIdx.x == 0 && it + 1 < total_it) issue(it + 1);
+      mbar_wait(bar + (it & 1), (uint32_t)((it >> 1) & 1));
+      const unsigned char* tb = tabs + (it & 1) * SLOT;
+      const uint2* t_scat = reinterpret_cast<const uint2*>(tb);
+      const float* t_cs = reinterpret_cast<const float*>(tb + N * 8);
+      const uint32_t* t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
+
+      float v[R];
+      // ---- x * B (sign XOR, exact)
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const uint32_t bits = __ldg(p.bmask + ((int64_t)e * W + w) * T + tid);
+      for (int w = 0; w < W; ++w) {
+        const uint32_t bits = t_bm[w * T + tid];
 #pragma unroll
-      for (int q = 0; q < 32 && 32 * w + q < R; ++q)
-        v[32 * w + q] = __uint_as_float(__float_as_uint(xr[32 * w + q]) ^ (((bits >> q) & 1u) << 31));
-    }
-    // ---- H (first)
-    butterflies<R, C::PL, C::PL>(v);
-    middle_rounds<C, 0, C::PL>(s, tid, gid, v);
-    // ---- Pi and G: scatter z1[j] * g[perm^-1[j]] to perm^-1[j]
-    {
-      const uint2* sc = p.scat + (int64_t)e * R * T + tid;
+        for (int q = 0; q < 32 && 32 * w + q < R; ++q)
+          v[32 * w + q] = __uint_as_float(__float_as_uint(xr[32 * w + q]) ^ (((bits >> q) & 1u) << 31));
+      }
+      // ---- H (first)
+      butterflies<R, C::PL, C::PL>(v);
+      middle_rounds<C, 0, C::PL>(s, tid, gid, v);
+      // ---- Pi and G: scatter z1[j] * g[perm^-1[j]] to perm^-1[j]
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const uint2 a = __ldg(sc + k * T);
+        const uint2 a = t_scat[k * T + tid];
         s[a.x] = v[k] * __uint_as_float(a.y);
       }
-    }
-    group_sync<T>(gid);
-    lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
-    group_sync<T>(gid);
-    // ---- H (second), ending in layout L
-    middle_rounds_then_L<C, 0, R>(s, tid, gid, v);
-    butterflies<R, C::PL, C::PL>(v);
-    // ---- C * scale, feature epilogue
-    const float* csp = p.cs + (int64_t)e * N;
+      group_sync<T>(gid);
+      lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
+      group_sync<T>(gid);
+      // ---- H (second), ending in layout L
+      middle_rounds_then_L<C, 0, R>(s, tid, gid, v);
+      butterflies<R, C::PL, C::PL>(v);
+      // ---- C * scale, feature epilogue
 #pragma unroll
-    for (int j = 0; j < R / 4; ++j) {
-      const int i0 = 4 * (int)tid + j * 4 * T;
-      const float4 c4 = __ldg(reinterpret_cast<const float4*>(csp + i0));
-      float z[4] = {v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]};
-      const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+      for (int j = 0; j < R / 4; ++j) {
+        const int i0 = 4 * (int)tid + j * 4 * T;
+        const float4 c4 = *reinterpret_cast<const float4*>(t_cs + i0);
+        float z[4] = {v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]};
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) z[c] = FOLD ? z[c] * cc[c] : (z[c] * cc[c]) * p.scale;
-      if (valid) {
-        float* o = orow + (int64_t)e * N + i0;
-        if constexpr (FEAT) {
-          float sn[4], cn[4];
+        for (int c = 0; c < 4; ++c) z[c] = FOLD ? z[c] * cc[c] : (z[c] * cc[c]) * p.scale;
+        if (valid) {
+          float* o = orow + (int64_t)e * N + i0;
+          if constexpr (FEAT) {
+            float sn[4], cn[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            sincos_fast(z[c], sn[c], cn[c]);
-            sn[c] *= p.norm;
-            cn[c] *= p.norm;
+            for (int c = 0; c < 4; ++c) {
+              sincos_fast(z[c], sn[c], cn[c]);
+              sn[c] *= p.norm;
+              cn[c] *= p.norm;
+            }
+            *reinterpret_cast<float4*>(o) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+            *reinterpret_cast<float4*>(o + p.D) = make_float4(sn[0], sn[1], sn[2], sn[3]);
+          } else {
+            *reinterpret_cast<float4*>(o) = make_float4(z[0], z[1], z[2], z[3]);
           }
-          *reinterpret_cast<float4*>(o) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-          *reinterpret_cast<float4*>(o + p.D) = make_float4(sn[0], sn[1], sn[2], sn[3]);
-        } else {
-          *reinterpret_cast<float4*>(o) = make_float4(z[0], z[1], z[2], z[3]);
         }
       }
     }
@@ -274,8 +323,6 @@ int prepare_cfg(const TablesView& tv, cudaStream_t st) {
   return check_launch("k_prepare");
 }
 
-int ff_logr(int logn);  // below
-
 int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st, bool validate) {
   const int64_t total = tv.n * tv.E;
   unsigned grid = (unsigned)((total + 255) / 256);
@@ -315,21 +362,23 @@ int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st,
 template <class C, bool FEAT, bool FOLD, bool VEC>
 int launch_ff(const FFParams& p, cudaStream_t st) {
   constexpr int ROWS = ff_rows_per_cta<C>();
-  const size_t smem = (size_t)ROWS * C::SMEM_FLOATS * sizeof(float);
+  const size_t smem = ff_smem_bytes<C>();
   auto kern = k_fastfood<C, FEAT, FOLD, VEC>;
-  if (smem > 48 * 1024)
+  static int occ = 0, sms = 0;  // per instantiation, per process (one device type)
+  if (occ == 0) {
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "fastfood smem"));
-  const int64_t blocks = (p.m + ROWS - 1) / ROWS;
-  FFParams q = p;
-  for (int64_t b0 = 0; b0 < blocks; b0 += (1ll << 30)) {
-    const int64_t nb = blocks - b0 < (1ll << 30) ? blocks - b0 : (1ll << 30);
-    q.m = p.m - b0 * ROWS;
-    q.out = p.out + b0 * ROWS * p.ldo;
-    if (p.rows) q.rows = p.rows + b0 * ROWS;
-    else q.x = p.x + b0 * ROWS * p.ldx;
-    kern<<<(unsigned)nb, C::T * ROWS, smem, st>>>(q);
+    int dev = 0;
+    MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
+    MCK_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms"));
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::T * ROWS, smem),
+                       "occupancy"));
+    if (occ < 1) occ = 1;
   }
+  const int64_t groups = (p.m + ROWS - 1) / ROWS;
+  int64_t grid = (int64_t)sms * occ;
+  if (grid > groups) grid = groups;
+  kern<<<(unsigned)grid, C::T * ROWS, smem, st>>>(p);
   return check_launch("k_fastfood");
 }
 

@@ -1,0 +1,25 @@
+"""Small driver for ncu captures: c2 expansion (4096-row batch) and the FWHT at a given length."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+import paper_1702_08159_b200 as P
+from paper_1702_08159_b200 import synthetic
+
+what = sys.argv[1] if len(sys.argv) > 1 else "ff"
+if what == "ff":
+    spec = P.FeatureMapSpec(784, 16, P.RBFMatern(2.0, 40), 42)
+    blocks = P.build_blocks(spec)
+    x = torch.from_numpy(synthetic.image_rows(4096, 784, 42)).cuda()
+    out = torch.empty((4096, 32768), device="cuda")
+    for _ in range(4):
+        P.feature_map_batch(spec, blocks, x, out=out)
+elif what == "fwht":
+    n = int(sys.argv[2])
+    buf = torch.randn(1 << 28, device="cuda").view(-1, n)
+    for _ in range(3):
+        P.wht_fast_batch(buf)
+torch.cuda.synchronize()
+print("done")
