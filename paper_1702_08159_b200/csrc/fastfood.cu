@@ -103,12 +103,11 @@ __global__ void k_prepare(const float* b, const float* g, const int32_t* perminv
 }
 
 // ---------------------------------------------------------------- sincos
-__device__ __forceinline__ void sincos_fast(float z, float& s, float& c) {
-  const float k = rintf(z * 0.159154943091895336f);
-  float r = fmaf(-k, 6.28318548202514648f, z);
-  r = fmaf(-k, -1.74845553146951720e-7f, r);
-  __sincosf(r, &s, &c);
-}
+// MUFU sin/cos work in turns on the fractional part of z/(2 pi); the only
+// error beyond the unit's ~2^-21 is the rounding of z/(2 pi), i.e. about
+// |z| * 2^-24 -- below the fp32 error of z itself, so no explicit range
+// reduction is needed.
+__device__ __forceinline__ void sincos_fast(float z, float& s, float& c) { __sincosf(z, &s, &c); }
 
 struct FFParams {
   const float* x;
@@ -130,8 +129,11 @@ struct FFParams {
 // Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
 // tables of iteration it+1 (next block, or block 0 of the next group) are in
 // flight while iteration it computes.
+template <class C>
+constexpr int ff_min_blocks() { return C::T * ff_rows_per_cta<C>() <= 256 ? 3 : 1; }
+
 template <class C, bool FEAT, bool FOLD, bool VEC>
-__global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>())
+__global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>(), ff_min_blocks<C>())
 k_fastfood(FFParams p) {
   constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
   constexpr int ROWS = ff_rows_per_cta<C>();
@@ -211,10 +213,15 @@ k_fastfood(FFParams p) {
       butterflies<R, C::PL, C::PL>(v);
       middle_rounds<C, 0, C::PL>(s, tid, gid, v);
       // ---- Pi and G: scatter z1[j] * g[perm^-1[j]] to perm^-1[j]
+      // table loads batched ahead of the stores: the compiler cannot hoist a
+      // shared load above a shared store to an unknown address by itself
 #pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const uint2 a = t_scat[k * T + tid];
-        s[a.x] = v[k] * __uint_as_float(a.y);
+      for (int k0 = 0; k0 < R; k0 += 8) {
+        uint2 a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + tid];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[a[q].x] = v[k0 + q] * __uint_as_float(a[q].y);
       }
       group_sync<T>(gid);
       lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
