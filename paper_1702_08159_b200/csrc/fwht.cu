@@ -107,32 +107,47 @@ int launch_rows(V* data, int64_t rows, cudaStream_t st) {
 }
 
 // Phase A of the large-n path: H_{N1} along the column index of the
-// [N1][N2] view, one thread per column, all N1 values in registers.
-template <int LOGN1, class V>
+// [N1][N2] view.  A thread owns VW adjacent columns (one 16/8/4-byte vector
+// per row of the view) with all N1 vectors in registers, and strides over the
+// chunk's columns (grid sized to the machine, not to the data).
+template <class V, int VW> struct VecT;
+template <> struct VecT<float, 4> { using T = float4; };
+template <> struct VecT<float, 2> { using T = float2; };
+template <> struct VecT<float, 1> { using T = float; };
+template <> struct VecT<double, 2> { using T = double2; };
+template <> struct VecT<double, 1> { using T = double; };
+
+__device__ __forceinline__ void vadd(float& a, float& b) { const float x = a; a = x + b; b = x - b; }
+__device__ __forceinline__ void vadd(double& a, double& b) { const double x = a; a = x + b; b = x - b; }
+__device__ __forceinline__ void vadd(float2& a, float2& b) { vadd(a.x, b.x); vadd(a.y, b.y); }
+__device__ __forceinline__ void vadd(double2& a, double2& b) { vadd(a.x, b.x); vadd(a.y, b.y); }
+__device__ __forceinline__ void vadd(float4& a, float4& b) {
+  vadd(a.x, b.x); vadd(a.y, b.y); vadd(a.z, b.z); vadd(a.w, b.w);
+}
+
+template <int LOGN1, int VW, class V>
 __global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, int64_t rows,
                                                         int n2) {
+  using VT = typename VecT<V, VW>::T;
   constexpr int N1 = 1 << LOGN1;
-  const int64_t col_blocks = n2 / 256;
-  const int64_t row = blockIdx.x / col_blocks;
-  const int64_t col = (blockIdx.x % col_blocks) * 256 + threadIdx.x;
-  if (row >= rows) return;
-  V* p = data + row * (int64_t)N1 * n2 + col;
-  V v[N1];
+  const int64_t vcols = n2 / VW;
+  const int64_t total = rows * vcols;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / vcols;
+    VT* p = reinterpret_cast<VT*>(data + row * (int64_t)N1 * n2) + (t % vcols);
+    VT v[N1];
 #pragma unroll
-  for (int i = 0; i < N1; ++i) v[i] = p[(int64_t)i * n2];
+    for (int i = 0; i < N1; ++i) v[i] = p[(int64_t)i * vcols];
 #pragma unroll
-  for (int h = 1; h < N1; h <<= 1) {
+    for (int h = 1; h < N1; h <<= 1) {
 #pragma unroll
-    for (int i = 0; i < N1; ++i) {
-      if (!(i & h)) {
-        V a = v[i], b = v[i | h];
-        v[i] = a + b;
-        v[i | h] = a - b;
-      }
+      for (int i = 0; i < N1; ++i)
+        if (!(i & h)) vadd(v[i], v[i | h]);
     }
-  }
 #pragma unroll
-  for (int i = 0; i < N1; ++i) p[(int64_t)i * n2] = v[i];
+    for (int i = 0; i < N1; ++i) p[(int64_t)i * vcols] = v[i];
+  }
 }
 
 template <class V>
@@ -157,17 +172,43 @@ int launch_rows_by_logn(V* data, int64_t rows, int logn, cudaStream_t st) {
   }
 }
 
+template <int LOGN1, int VW, class V>
+int launch_cols_t(V* data, int64_t rows, int n2, cudaStream_t st) {
+  const int64_t total = rows * (n2 / VW);
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  fwht_cols_kernel<LOGN1, VW, V><<<(unsigned)grid, 256, 0, st>>>(data, rows, n2);
+  return check_launch("fwht_cols_kernel");
+}
+
 template <class V>
 int launch_cols(V* data, int64_t rows, int logn1, int n2, cudaStream_t st) {
-  const int64_t grid = rows * (n2 / 256);
+  constexpr bool F = sizeof(V) == 4;
   switch (logn1) {
-#define MCK_COLS(L) \
-  case L: fwht_cols_kernel<L, V><<<(unsigned)grid, 256, 0, st>>>(data, rows, n2); break;
-    MCK_COLS(1) MCK_COLS(2) MCK_COLS(3) MCK_COLS(4) MCK_COLS(5) MCK_COLS(6)
-#undef MCK_COLS
+    case 1: return launch_cols_t<1, F ? 4 : 2, V>(data, rows, n2, st);
+    case 2: return launch_cols_t<2, F ? 4 : 2, V>(data, rows, n2, st);
+    case 3: return launch_cols_t<3, F ? 4 : 2, V>(data, rows, n2, st);
+    case 4: return launch_cols_t<4, F ? 4 : 2, V>(data, rows, n2, st);
+    case 5: return launch_cols_t<5, F ? 2 : 1, V>(data, rows, n2, st);
+    case 6: return launch_cols_t<6, 1, V>(data, rows, n2, st);
     default: return fail_value("internal: no column kernel for 2^%d", logn1);
   }
-  return check_launch("fwht_cols_kernel");
+}
+
+// Second stream used to overlap phase B of chunk k with phase A of chunk k+1.
+struct SideStreams {
+  cudaStream_t s[16] = {};
+};
+static SideStreams g_side;
+
+static int side_stream(cudaStream_t* out) {
+  int dev = 0;
+  MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
+  if (dev >= 16) return fail_value("device index out of range");
+  if (!g_side.s[dev])
+    MCK_TRY(check_cuda(cudaStreamCreateWithFlags(&g_side.s[dev], cudaStreamNonBlocking), "stream"));
+  *out = g_side.s[dev];
+  return MCK_OK;
 }
 
 // tiny rows: one thread per row, serial butterflies (n <= 4)
@@ -195,16 +236,33 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
   const int logn2 = 14, logn1 = logn - logn2;
   if (logn1 > 6) return fail_value("length %lld exceeds the supported maximum 2^20", (long long)n);
   const int n2 = 1 << logn2;
-  // chunk so that one chunk (<= 24 MiB) stays L2-resident between phases
+  // Chunks of <= 24 MiB: phase B of a chunk finds phase A's output in L2.
+  // Phase A of chunk k+1 (main stream) overlaps phase B of chunk k (side
+  // stream); the caller's stream waits for the last phase B.
   int64_t chunk = (24ll << 20) / (n * (int64_t)sizeof(V));
   if (chunk < 1) chunk = 1;
-  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+  cudaStream_t side;
+  MCK_TRY(side_stream(&side));
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  MCK_TRY(check_cuda(cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming), "event"));
+  MCK_TRY(check_cuda(cudaEventRecord(ev_b, st), "event"));
+  MCK_TRY(check_cuda(cudaStreamWaitEvent(side, ev_b, 0), "wait"));  // side starts after prior work
+  int rc = MCK_OK;
+  for (int64_t r0 = 0; r0 < rows && rc == MCK_OK; r0 += chunk) {
     const int64_t nr = rows - r0 < chunk ? rows - r0 : chunk;
     V* p = data + r0 * n;
-    MCK_TRY(launch_cols<V>(p, nr, logn1, n2, st));
-    MCK_TRY(launch_rows_by_logn<V>(p, nr << logn1, logn2, st));
+    rc = launch_cols<V>(p, nr, logn1, n2, st);
+    if (rc != MCK_OK) break;
+    if (!ev_a) rc = check_cuda(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming), "event");
+    if (rc == MCK_OK) rc = check_cuda(cudaEventRecord(ev_a, st), "event");
+    if (rc == MCK_OK) rc = check_cuda(cudaStreamWaitEvent(side, ev_a, 0), "wait");
+    if (rc == MCK_OK) rc = launch_rows_by_logn<V>(p, nr << logn1, logn2, side);
   }
-  return MCK_OK;
+  if (rc == MCK_OK) rc = check_cuda(cudaEventRecord(ev_b, side), "event");
+  if (rc == MCK_OK) rc = check_cuda(cudaStreamWaitEvent(st, ev_b, 0), "wait");
+  if (ev_a) cudaEventDestroy(ev_a);
+  cudaEventDestroy(ev_b);
+  return rc;
 }
 
 // ---------------------------------------------------------------- parity
