@@ -289,6 +289,23 @@ def extras(args, P, torch, dev, hbm):
     out["c0_features"] = {"ms_per_batch": round(ms0, 4),
                           "features_per_s": 1000 * 16384 / (ms0 / 1e3),
                           "GBps": round(1000 * (3136 + 65536) / (ms0 / 1e3) / 1e9, 1)}
+    # config 4 expansion alone (n = 16384, E = 32, sigma = 4): 256 rows ->
+    # 2^20 features/row materialised (the fused classifier path is K6)
+    spec4 = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4)
+    t0 = time.perf_counter()
+    b4 = P.build_blocks(spec4)
+    torch.cuda.synchronize()
+    setup4 = time.perf_counter() - t0
+    x4 = torch.randn((256, 16384), generator=torch.Generator(device=dev).manual_seed(7),
+                     device=dev)
+    o4 = torch.empty((256, 1 << 20), device=dev)
+    P.feature_map_batch(spec4, b4, x4, normalize=False, out=o4)
+    ms4 = time_cuda(lambda: P.feature_map_batch(spec4, b4, x4, normalize=False, out=o4), 5, torch)
+    out["c4_expansion"] = {"rows": 256, "ms": round(ms4, 4),
+                           "features_per_s": 256 * (1 << 20) / (ms4 / 1e3),
+                           "GBps": round(256 * (65536 + 4 * (1 << 20)) / (ms4 / 1e3) / 1e9, 1),
+                           "build_blocks_s": round(setup4, 3)}
+    del o4, x4
     # config 3: one training epoch (60 steps of 1000 rows + 10k-row evaluation)
     x, y = synthetic.class_images(60000, 784, 10, seed=1234)
     xt, yt = synthetic.class_images(10000, 784, 10, seed=1234, sample_seed=99)

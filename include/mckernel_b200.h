@@ -133,10 +133,11 @@ int mck_head_forward(const float* phi, int64_t m, int64_t num_features, int64_t 
                      void* scratch, void* stream);
 
 /* linear_model.py:126-131 gradients -- dW = delta^T phi (C x F, f64) and
- * db = sum_r delta_r (C).  Overwrites dw/db. */
+ * db = sum_r delta_r (C).  Overwrites dw/db.  `scratch` as for
+ * mck_head_forward (mck_head_scratch_bytes(m, F, C) bytes). */
 int mck_head_backward(const float* phi, int64_t m, int64_t num_features, int64_t ldphi,
                       const double* delta, int32_t num_classes, double* dw,
-                      double* db, void* stream);
+                      double* db, void* scratch, void* stream);
 
 /* linear_model.py:134-142 sgd_step -- W -= lr*(dW + 2*l2*W); b -= lr*db. */
 int mck_head_sgd_update(double* w, double* b, const double* dw, const double* db,
@@ -147,7 +148,8 @@ int mck_head_sgd_update(double* w, double* b, const double* dw, const double* db
  * b -= lr*sum(delta), without materialising dW. */
 int mck_head_backward_sgd(const float* phi, int64_t m, int64_t num_features,
                           int64_t ldphi, const double* delta, int32_t num_classes,
-                          double* w, double* b, double lr, double l2, void* stream);
+                          double* w, double* b, double lr, double l2, void* scratch,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -55,9 +55,9 @@ int fastfood_run(const TablesView&, int32_t, double, const float*, int64_t, int6
 int head_forward(const float*, int64_t, int64_t, int64_t, const double*, const double*, int32_t,
                  const int32_t*, const int32_t*, int64_t, double*, double*, double*, int64_t*, void*, cudaStream_t);
 int head_backward(const float*, int64_t, int64_t, int64_t, const double*, int32_t, double*,
-                  double*, cudaStream_t);
+                  double*, void*, cudaStream_t);
 int head_backward_sgd(const float*, int64_t, int64_t, int64_t, const double*, int32_t, double*,
-                      double*, double, double, cudaStream_t);
+                      double*, double, double, void*, cudaStream_t);
 int head_sgd_update(double*, double*, const double*, const double*, int64_t, int32_t, double,
                     double, cudaStream_t);
 int64_t head_scratch_bytes(int64_t, int64_t, int32_t);
@@ -243,9 +243,9 @@ int mck_head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const d
 }
 
 int mck_head_backward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
-                      int32_t C, double* dw, double* db, void* st) {
+                      int32_t C, double* dw, double* db, void* scratch, void* st) {
   if (F < 1 || ld < F) return fail_value("bad feature geometry");
-  return head_backward(phi, m, F, ld, delta, C, dw, db, S(st));
+  return head_backward(phi, m, F, ld, delta, C, dw, db, scratch, S(st));
 }
 
 int mck_head_sgd_update(double* w, double* b, const double* dw, const double* db, int64_t F,
@@ -255,10 +255,11 @@ int mck_head_sgd_update(double* w, double* b, const double* dw, const double* db
 }
 
 int mck_head_backward_sgd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
-                          int32_t C, double* w, double* b, double lr, double l2, void* st) {
+                          int32_t C, double* w, double* b, double lr, double l2, void* scratch,
+                          void* st) {
   if (F < 1 || ld < F) return fail_value("bad feature geometry");
   if (!(lr > 0.0)) return fail_value("learning rate must be positive");
-  return head_backward_sgd(phi, m, F, ld, delta, C, w, b, lr, l2, S(st));
+  return head_backward_sgd(phi, m, F, ld, delta, C, w, b, lr, l2, scratch, S(st));
 }
 
 }  // extern "C"

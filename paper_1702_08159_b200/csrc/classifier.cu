@@ -1,92 +1,128 @@
 // K4/K5 -- softmax head on the expanded features (replaces
 // linear_model.py:95-142: forward_batch, loss, gradients, sgd_step).
 //
-// The head is a 10-class contraction over 16,384 features: ~5 FLOP per byte
-// of phi, i.e. bound by reading phi (which the training step keeps L2
-// resident), not by math.  It is written for CUDA cores in float64 like the
-// reference (float64 W, logits and gradients over float32 features) and all
-// reductions run in a fixed order, so training is bit-reproducible.
+// The head is a 10-class contraction over 16,384 features -- a tall-skinny
+// GEMM bound by reading phi (kept L2-resident by the training step), not by
+// math.  It runs on CUDA cores in float64 like the reference (float64 W,
+// logits and gradients over float32 features).  Register blocking: a warp
+// carries 4 rows x C classes of partial logits over a 1,024-feature chunk
+// whose W slice sits in shared memory (forward); a thread carries 4 features
+// x C classes of dW over a row range with delta in shared memory (backward).
+// Every reduction (split-K logits, row splits of dW, db, loss, hits) runs in a
+// fixed order, so training is bit-reproducible.
+#include <type_traits>
+
 #include "mck_common.cuh"
 
 namespace mck {
 
 constexpr int kMaxClasses = 16;
-constexpr int kFwdFeat = 256;   // features per split in the forward pass
-constexpr int kFwdRows = 32;    // rows per CTA in the forward pass
-constexpr int kBwdFeat = 128;   // features per CTA in the backward pass
-constexpr int kBwdRowChunk = 256;
+constexpr int kFwdK = 1024;     // features per forward CTA (W slice in smem)
+constexpr int kFwdRowsPerWarp = 4;
+constexpr int kFwdWarps = 8;
+constexpr int kFwdRows = kFwdRowsPerWarp * kFwdWarps;  // rows per forward CTA
+constexpr int kBwdFeatPerThread = 4;
+constexpr int kBwdThreads = 256;
+constexpr int kBwdK = kBwdFeatPerThread * kBwdThreads;  // features per backward CTA
+constexpr int kBwdRowChunk = 128;
 
 struct HeadScratch {
-  double* partial;  // [KS][m][C]
+  double* partial;  // [KS][m][C]   split-K logits
   double* rowloss;  // [m]
   int32_t* rowhit;  // [m]
+  double* dwpart;   // [RS][C][F]   row-split dW
 };
 
-inline int64_t head_splits(int64_t F) { return (F + kFwdFeat - 1) / kFwdFeat; }
+inline int64_t head_ksplits(int64_t F) { return (F + kFwdK - 1) / kFwdK; }
+inline int64_t head_rsplits(int64_t m, int64_t F, int32_t C) {
+  int64_t rs = (int64_t(1) << 22) / ((int64_t)C * F);  // keep dW partials <= 32 MB
+  if (rs > 16) rs = 16;
+  if (rs > (m + 63) / 64) rs = (m + 63) / 64;
+  return rs < 1 ? 1 : rs;
+}
 
 inline int64_t head_layout(int64_t m, int64_t F, int32_t C, char* base, HeadScratch* hs) {
-  const int64_t KS = head_splits(F);
   auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   int64_t off = 0;
   HeadScratch h{};
   h.partial = (double*)(base ? base + off : nullptr);
-  off += al(KS * m * C * 8);
+  off += al(head_ksplits(F) * m * C * 8);
   h.rowloss = (double*)(base ? base + off : nullptr);
   off += al(m * 8);
   h.rowhit = (int32_t*)(base ? base + off : nullptr);
   off += al(m * 4);
+  h.dwpart = (double*)(base ? base + off : nullptr);
+  off += al(head_rsplits(m, F, C) * C * F * 8);
   if (hs) *hs = h;
   return off;
 }
 
-// partial[ks][r][c] = sum_{f in split ks} phi[r][f] * W[c][f]
-__global__ void __launch_bounds__(256) k_head_fwd_partial(const float* __restrict__ phi, int64_t m,
-                                                          int64_t F, int64_t ld,
-                                                          const double* __restrict__ w, int C,
-                                                          double* __restrict__ partial) {
-  __shared__ double ws[kMaxClasses][kFwdFeat];
+// partial[ks][r][c] = sum_{f in chunk ks} phi[r][f] * W[c][f]
+template <int NC>
+__global__ void __launch_bounds__(kFwdWarps * 32) k_head_fwd(const float* __restrict__ phi,
+                                                             int64_t m, int64_t F, int64_t ld,
+                                                             const double* __restrict__ w,
+                                                             double* __restrict__ partial) {
+  extern __shared__ __align__(16) double ws[];  // [NC][kFwdK]
   const int ks = blockIdx.y;
-  const int64_t f0 = (int64_t)ks * kFwdFeat;
-  const int nf = (int)((F - f0) < kFwdFeat ? (F - f0) : kFwdFeat);
-  for (int t = threadIdx.x; t < C * kFwdFeat; t += blockDim.x) {
-    const int c = t / kFwdFeat, f = t % kFwdFeat;
-    ws[c][f] = f < nf ? w[(int64_t)c * F + f0 + f] : 0.0;
+  const int64_t f0 = (int64_t)ks * kFwdK;
+  const int nf = (int)((F - f0) < kFwdK ? (F - f0) : kFwdK);
+  for (int t = threadIdx.x; t < NC * kFwdK; t += blockDim.x) {
+    const int c = t / kFwdK, f = t % kFwdK;
+    ws[t] = f < nf ? w[(int64_t)c * F + f0 + f] : 0.0;
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rr = warp; rr < kFwdRows; rr += 8) {
-    const int64_t r = (int64_t)blockIdx.x * kFwdRows + rr;
-    if (r >= m) break;
-    double acc[kMaxClasses];
+  const int64_t r0 = (int64_t)blockIdx.x * kFwdRows + warp * kFwdRowsPerWarp;
+  double acc[kFwdRowsPerWarp][NC];
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0;
-    const float* pr = phi + r * ld + f0;
-    for (int f = lane; f < nf; f += 32) {
-      const double x = (double)pr[f];
+  for (int q = 0; q < kFwdRowsPerWarp; ++q)
 #pragma unroll
-      for (int c = 0; c < kMaxClasses; ++c)
-        if (c < C) acc[c] = fma(x, ws[c][f], acc[c]);
+    for (int c = 0; c < NC; ++c) acc[q][c] = 0.0;
+  const float* pr[kFwdRowsPerWarp];
+#pragma unroll
+  for (int q = 0; q < kFwdRowsPerWarp; ++q) {
+    const int64_t r = r0 + q < m ? r0 + q : m - 1;  // clamp: duplicates are discarded
+    pr[q] = phi + r * ld + f0;
+  }
+  for (int f = lane; f < nf; f += 32) {
+    double x[kFwdRowsPerWarp];
+#pragma unroll
+    for (int q = 0; q < kFwdRowsPerWarp; ++q) x[q] = (double)__ldg(pr[q] + f);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double wc = ws[c * kFwdK + f];
+#pragma unroll
+      for (int q = 0; q < kFwdRowsPerWarp; ++q) acc[q][c] = fma(x[q], wc, acc[q][c]);
     }
+  }
 #pragma unroll
-    for (int c = 0; c < kMaxClasses; ++c) {
-      if (c < C) {
-        double v = acc[c];
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        if (lane == 0) partial[((int64_t)ks * m + r) * C + c] = v;
-      }
+  for (int q = 0; q < kFwdRowsPerWarp; ++q) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double v = acc[q][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      acc[q][c] = v;
     }
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kFwdRowsPerWarp; ++q)
+      if (r0 + q < m)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) partial[((int64_t)ks * m + r0 + q) * NC + c] = acc[q][c];
   }
 }
 
 // logits -> stable softmax (linear_model.py:79-83) -> loss / delta / argmax
 __global__ void k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
                                const double* __restrict__ b, const int32_t* __restrict__ labels,
-                               const int32_t* __restrict__ label_index, int64_t m_total, double* probs, double* delta, double* rowloss,
-                               int32_t* rowhit) {
+                               const int32_t* __restrict__ label_index, int64_t m_total,
+                               double* probs, double* delta, double* rowloss, int32_t* rowhit) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   double z[kMaxClasses];
@@ -142,21 +178,42 @@ __global__ void k_head_reduce(const double* rowloss, const int32_t* rowhit, int6
   }
 }
 
+template <int NC>
+int launch_fwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
+               double* partial, cudaStream_t st) {
+  const size_t smem = (size_t)NC * kFwdK * sizeof(double);
+  auto kern = k_head_fwd<NC>;
+  if (smem > 48 * 1024)
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "head fwd smem"));
+  dim3 grid((unsigned)((m + kFwdRows - 1) / kFwdRows), (unsigned)head_ksplits(F));
+  kern<<<grid, kFwdWarps * 32, smem, st>>>(phi, m, F, ld, w, partial);
+  return check_launch("k_head_fwd");
+}
+
 int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
                  const double* b, int32_t C, const int32_t* labels, const int32_t* label_index,
-                 int64_t m_total, double* probs, double* delta, double* loss_sum, int64_t* hits, void* scratch,
-                 cudaStream_t st) {
+                 int64_t m_total, double* probs, double* delta, double* loss_sum, int64_t* hits,
+                 void* scratch, cudaStream_t st) {
   if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
   if (m == 0) return MCK_OK;
   HeadScratch hs;
   head_layout(m, F, C, (char*)scratch, &hs);
-  const int64_t KS = head_splits(F);
-  dim3 grid((unsigned)((m + kFwdRows - 1) / kFwdRows), (unsigned)KS);
-  k_head_fwd_partial<<<grid, 256, 0, st>>>(phi, m, F, ld, w, C, hs.partial);
-  MCK_TRY(check_launch("k_head_fwd_partial"));
-  k_head_softmax<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(hs.partial, KS, m, C, b, labels,
-                                                              label_index, m_total, probs, delta, hs.rowloss,
-                                                              hs.rowhit);
+  auto fwd = [&](auto nc) {
+    return launch_fwd<decltype(nc)::value>(phi, m, F, ld, w, hs.partial, st);
+  };
+  int rc;
+  switch (C) {
+#define MCK_F(N) case N: rc = fwd(std::integral_constant<int, N>{}); break;
+    MCK_F(2) MCK_F(3) MCK_F(4) MCK_F(5) MCK_F(6) MCK_F(7) MCK_F(8) MCK_F(9) MCK_F(10)
+    MCK_F(11) MCK_F(12) MCK_F(13) MCK_F(14) MCK_F(15) MCK_F(16)
+#undef MCK_F
+    default: return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  }
+  MCK_TRY(rc);
+  k_head_softmax<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+      hs.partial, head_ksplits(F), m, C, b, labels, label_index, m_total, probs, delta,
+      hs.rowloss, hs.rowhit);
   MCK_TRY(check_launch("k_head_softmax"));
   if (labels && (loss_sum || hits)) {
     k_head_reduce<<<1, 1024, 0, st>>>(hs.rowloss, hs.rowhit, m, loss_sum, hits);
@@ -165,81 +222,136 @@ int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const doubl
   return MCK_OK;
 }
 
-// dW[c][f] = sum_r delta[r][c] * phi[r][f]; optionally fused SGD update.
-template <bool UPDATE>
-__global__ void __launch_bounds__(kBwdFeat) k_head_bwd(const float* __restrict__ phi, int64_t m,
-                                                       int64_t F, int64_t ld,
-                                                       const double* __restrict__ delta, int C,
-                                                       double* dw, double* w, double lr,
-                                                       double l2) {
-  __shared__ double sd[kBwdRowChunk][kMaxClasses];
-  const int64_t f = (int64_t)blockIdx.x * kBwdFeat + threadIdx.x;
-  double acc[kMaxClasses];
+// dwpart[rs][c][f] = sum_{r in split rs} delta[r][c] * phi[r][f]
+template <int NC>
+__global__ void __launch_bounds__(kBwdThreads) k_head_bwd(const float* __restrict__ phi,
+                                                          int64_t m, int64_t F, int64_t ld,
+                                                          const double* __restrict__ delta,
+                                                          int64_t rows_per_split,
+                                                          double* __restrict__ dwpart) {
+  __shared__ double sd[kBwdRowChunk][NC];
+  const int rs = blockIdx.y;
+  const int64_t rbeg = (int64_t)rs * rows_per_split;
+  const int64_t rend = rbeg + rows_per_split < m ? rbeg + rows_per_split : m;
+  const int64_t fb = (int64_t)blockIdx.x * kBwdK + threadIdx.x;
+  double acc[kBwdFeatPerThread][NC];
 #pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) acc[c] = 0.0;
-  for (int64_t r0 = 0; r0 < m; r0 += kBwdRowChunk) {
-    const int nr = (int)(m - r0 < kBwdRowChunk ? m - r0 : kBwdRowChunk);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nr * kMaxClasses; t += blockDim.x) {
-      const int rr = t / kMaxClasses, c = t % kMaxClasses;
-      sd[rr][c] = c < C ? delta[(r0 + rr) * C + c] : 0.0;
-    }
-    __syncthreads();
-    if (f < F) {
-      const float* pp = phi + r0 * ld + f;
-#pragma unroll 4
-      for (int rr = 0; rr < nr; ++rr) {
-        const double x = (double)pp[(int64_t)rr * ld];
+  for (int j = 0; j < kBwdFeatPerThread; ++j)
 #pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c)
-          if (c < C) acc[c] = fma(sd[rr][c], x, acc[c]);
+    for (int c = 0; c < NC; ++c) acc[j][c] = 0.0;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kBwdRowChunk) {
+    const int nr = (int)(rend - r0 < kBwdRowChunk ? rend - r0 : kBwdRowChunk);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nr * NC; t += blockDim.x) sd[t / NC][t % NC] = delta[r0 * NC + t];
+    __syncthreads();
+    const float* pp = phi + r0 * ld;
+#pragma unroll 2
+    for (int rr = 0; rr < nr; ++rr) {
+      double x[kBwdFeatPerThread];
+#pragma unroll
+      for (int j = 0; j < kBwdFeatPerThread; ++j) {
+        const int64_t f = fb + j * kBwdThreads;
+        x[j] = f < F ? (double)__ldg(pp + (int64_t)rr * ld + f) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double d = sd[rr][c];
+#pragma unroll
+        for (int j = 0; j < kBwdFeatPerThread; ++j) acc[j][c] = fma(d, x[j], acc[j][c]);
       }
     }
   }
-  if (f >= F) return;
 #pragma unroll
-  for (int c = 0; c < kMaxClasses; ++c) {
-    if (c < C) {
-      if constexpr (UPDATE) {
-        double g = acc[c];
-        const double wv = w[(int64_t)c * F + f];
-        if (l2 != 0.0) g += 2.0 * l2 * wv;
-        w[(int64_t)c * F + f] = wv - lr * g;
-      } else {
-        dw[(int64_t)c * F + f] = acc[c];
-      }
+  for (int j = 0; j < kBwdFeatPerThread; ++j) {
+    const int64_t f = fb + j * kBwdThreads;
+    if (f < F)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) dwpart[((int64_t)rs * NC + c) * F + f] = acc[j][c];
+  }
+}
+
+// dW = sum over row splits (fixed order); optionally W -= lr*(dW + 2*l2*W)
+__global__ void k_head_dw_finish(const double* __restrict__ dwpart, int64_t RS, int64_t total,
+                                 double* dw, double* w, double lr, double l2) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    for (int64_t s = 0; s < RS; ++s) g += dwpart[s * total + t];
+    if (w) {
+      const double wv = w[t];
+      if (l2 != 0.0) g += 2.0 * l2 * wv;
+      w[t] = wv - lr * g;
+    } else {
+      dw[t] = g;
     }
   }
 }
 
-// db[c] = sum_r delta[r][c] (fixed order), optional update b -= lr*db
+// db[c] = sum_r delta[r][c] in a fixed order; optionally b -= lr*db.  One CTA per class.
 __global__ void k_head_db(const double* delta, int64_t m, int C, double* db, double* b, double lr) {
-  const int c = threadIdx.x;
-  if (c >= C) return;
-  double s = 0.0;
-  for (int64_t r = 0; r < m; ++r) s += delta[r * C + c];
-  if (db) db[c] = s;
-  if (b) b[c] -= lr * s;
+  __shared__ double s[256];
+  const int c = blockIdx.x;
+  double a = 0.0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) a += delta[r * C + c];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (db) db[c] = s[0];
+    if (b) b[c] -= lr * s[0];
+  }
+}
+
+template <int NC>
+int launch_bwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
+               const HeadScratch& hs, int64_t RS, cudaStream_t st) {
+  const int64_t rows_per_split = (m + RS - 1) / RS;
+  dim3 grid((unsigned)((F + kBwdK - 1) / kBwdK), (unsigned)RS);
+  k_head_bwd<NC><<<grid, kBwdThreads, 0, st>>>(phi, m, F, ld, delta, rows_per_split, hs.dwpart);
+  return check_launch("k_head_bwd");
+}
+
+static int head_bwd_common(const float* phi, int64_t m, int64_t F, int64_t ld,
+                           const double* delta, int32_t C, double* dw, double* db, double* w,
+                           double* b, double lr, double l2, void* scratch, cudaStream_t st) {
+  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  if (m == 0) return MCK_OK;
+  HeadScratch hs;
+  head_layout(m, F, C, (char*)scratch, &hs);
+  const int64_t RS = head_rsplits(m, F, C);
+  auto bwd = [&](auto nc) {
+    return launch_bwd<decltype(nc)::value>(phi, m, F, ld, delta, hs, RS, st);
+  };
+  int rc;
+  switch (C) {
+#define MCK_B(N) case N: rc = bwd(std::integral_constant<int, N>{}); break;
+    MCK_B(2) MCK_B(3) MCK_B(4) MCK_B(5) MCK_B(6) MCK_B(7) MCK_B(8) MCK_B(9) MCK_B(10)
+    MCK_B(11) MCK_B(12) MCK_B(13) MCK_B(14) MCK_B(15) MCK_B(16)
+#undef MCK_B
+    default: return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  }
+  MCK_TRY(rc);
+  const int64_t total = (int64_t)C * F;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  k_head_dw_finish<<<(unsigned)grid, 256, 0, st>>>(hs.dwpart, RS, total, dw, w, lr, l2);
+  MCK_TRY(check_launch("k_head_dw_finish"));
+  k_head_db<<<C, 256, 0, st>>>(delta, m, C, db, b, lr);
+  return check_launch("k_head_db");
 }
 
 int head_backward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
-                  int32_t C, double* dw, double* db, cudaStream_t st) {
-  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
-  const unsigned grid = (unsigned)((F + kBwdFeat - 1) / kBwdFeat);
-  k_head_bwd<false><<<grid, kBwdFeat, 0, st>>>(phi, m, F, ld, delta, C, dw, nullptr, 0.0, 0.0);
-  MCK_TRY(check_launch("k_head_bwd"));
-  k_head_db<<<1, 32, 0, st>>>(delta, m, C, db, nullptr, 0.0);
-  return check_launch("k_head_db");
+                  int32_t C, double* dw, double* db, void* scratch, cudaStream_t st) {
+  return head_bwd_common(phi, m, F, ld, delta, C, dw, db, nullptr, nullptr, 0.0, 0.0, scratch, st);
 }
 
 int head_backward_sgd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
-                      int32_t C, double* w, double* b, double lr, double l2, cudaStream_t st) {
-  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
-  const unsigned grid = (unsigned)((F + kBwdFeat - 1) / kBwdFeat);
-  k_head_bwd<true><<<grid, kBwdFeat, 0, st>>>(phi, m, F, ld, delta, C, nullptr, w, lr, l2);
-  MCK_TRY(check_launch("k_head_bwd_sgd"));
-  k_head_db<<<1, 32, 0, st>>>(delta, m, C, nullptr, b, lr);
-  return check_launch("k_head_db");
+                      int32_t C, double* w, double* b, double lr, double l2, void* scratch,
+                      cudaStream_t st) {
+  return head_bwd_common(phi, m, F, ld, delta, C, nullptr, nullptr, w, b, lr, l2, scratch, st);
 }
 
 __global__ void k_sgd(double* w, double* b, const double* dw, const double* db, int64_t F, int C,

@@ -37,8 +37,14 @@ constexpr int tab_bytes() { return C::N * 8 + C::N * 4 + bm_stride<C>() * 4; }
 template <class C>
 constexpr int tab_slot() { return (tab_bytes<C>() + 127) & ~127; }
 template <class C>
+constexpr size_t ff_rows_bytes() { return (size_t)ff_rows_per_cta<C>() * C::SMEM_FLOATS * 4; }
+// Tables are staged when both buffers fit next to the row buffers (n <= 4096);
+// larger n (c4: 197 KB of tables per block) reads them through L2.
+template <class C>
+constexpr bool ff_staged() { return 128 + 2 * (size_t)tab_slot<C>() + ff_rows_bytes<C>() <= 200 * 1024; }
+template <class C>
 constexpr size_t ff_smem_bytes() {
-  return 128 + 2 * (size_t)tab_slot<C>() + (size_t)ff_rows_per_cta<C>() * C::SMEM_FLOATS * 4;
+  return ff_staged<C>() ? 128 + 2 * (size_t)tab_slot<C>() + ff_rows_bytes<C>() : ff_rows_bytes<C>();
 }
 
 
@@ -138,12 +144,13 @@ k_fastfood(FFParams p) {
   constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
   constexpr int ROWS = ff_rows_per_cta<C>();
   constexpr int SLOT = tab_slot<C>();
+  constexpr bool STAGED = ff_staged<C>();
   extern __shared__ __align__(128) unsigned char ff_smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(ff_smem);
   unsigned char* tabs = ff_smem + 128;
   const int gid = threadIdx.x / T;
   const uint32_t tid = threadIdx.x % T;
-  float* s = reinterpret_cast<float*>(ff_smem + 128 + 2 * SLOT) + gid * C::SMEM_FLOATS;
+  float* s = reinterpret_cast<float*>(ff_smem + (STAGED ? 128 + 2 * SLOT : 0)) + gid * C::SMEM_FLOATS;
   constexpr uint32_t P0 = C::mid_regs(0);
 
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
@@ -159,13 +166,15 @@ k_fastfood(FFParams p) {
     bulk_g2s(dst + N * 8, p.cs + (int64_t)e * N, N * 4, b);
     bulk_g2s(dst + N * 12, p.bmask + (int64_t)e * bm_stride<C>(), bm_stride<C>() * 4, b);
   };
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
-    fence_mbar_init();
+  if (STAGED) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && total_it > 0) issue(0);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && total_it > 0) issue(0);
 
   for (int64_t gi = 0; gi < my_groups; ++gi) {
     const int64_t row = (blockIdx.x + gi * gridDim.x) * ROWS + gid;
@@ -192,13 +201,22 @@ k_fastfood(FFParams p) {
 
     for (int e = 0; e < p.E; ++e) {
       const int64_t it = gi * p.E + e;
-      __syncthreads();  // buffer (it+1)&1 (read at it-1) is free
-      if (threadIdx.x == 0 && it + 1 < total_it) issue(it + 1);
-      mbar_wait(bar + (it & 1), (uint32_t)((it >> 1) & 1));
-      const unsigned char* tb = tabs + (it & 1) * SLOT;
-      const uint2* t_scat = reinterpret_cast<const uint2*>(tb);
-      const float* t_cs = reinterpret_cast<const float*>(tb + N * 8);
-      const uint32_t* t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
+      const uint2* t_scat;
+      const float* t_cs;
+      const uint32_t* t_bm;
+      if constexpr (STAGED) {
+        __syncthreads();  // buffer (it+1)&1 (read at it-1) is free
+        if (threadIdx.x == 0 && it + 1 < total_it) issue(it + 1);
+        mbar_wait(bar + (it & 1), (uint32_t)((it >> 1) & 1));
+        const unsigned char* tb = tabs + (it & 1) * SLOT;
+        t_scat = reinterpret_cast<const uint2*>(tb);
+        t_cs = reinterpret_cast<const float*>(tb + N * 8);
+        t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
+      } else {
+        t_scat = p.scat + (int64_t)e * N;
+        t_cs = p.cs + (int64_t)e * N;
+        t_bm = p.bmask + (int64_t)e * bm_stride<C>();
+      }
 
       float v[R];
       // ---- x * B (sign XOR, exact)

@@ -204,7 +204,7 @@ def gradients(model: SoftmaxModel, x, labels, l2_lambda: float = 0.0):
     db = torch.empty_like(model.b)
     nat.call("mck_head_backward", nat.ptr(phi), m, model.num_features, phi.stride(0),
              nat.ptr(head.delta), model.num_classes, nat.ptr(dw), nat.ptr(db),
-             nat.stream_handle(model.w.device))
+             nat.ptr(head.scratch), nat.stream_handle(model.w.device))
     if l2_lambda:
         dw += 2.0 * l2_lambda * model.w
     return dw, db
@@ -284,12 +284,14 @@ class Trainer:
                 self.step_loss[s] += mg * cfg.l2_lambda * (self.model.w * self.model.w).sum()
             nat.call("mck_head_backward_sgd", nat.ptr(phi), ml, self.F, phi.stride(0),
                      nat.ptr(self.head.delta), self.C, nat.ptr(self.model.w),
-                     nat.ptr(self.model.b), float(cfg.learning_rate), float(cfg.l2_lambda), st)
+                     nat.ptr(self.model.b), float(cfg.learning_rate), float(cfg.l2_lambda),
+                     nat.ptr(self.head.scratch), st)
             return
         b = self.bucket
         if ml > 0:
             nat.call("mck_head_backward", nat.ptr(phi), ml, self.F, phi.stride(0),
-                     nat.ptr(self.head.delta), self.C, nat.ptr(b.dw), nat.ptr(b.db), st)
+                     nat.ptr(self.head.delta), self.C, nat.ptr(b.dw), nat.ptr(b.db),
+                     nat.ptr(self.head.scratch), st)
         else:
             b.flat.zero_()
         b.allreduce()

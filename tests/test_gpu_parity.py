@@ -224,6 +224,27 @@ class TestFeatures:
         raw = P.feature_map_batch(spec, blocks, x[:2], normalize=False)
         assert np.abs(raw - z["raw"]).max() <= 1e-4
 
+    def test_config4_rows(self, cuda):
+        # n = 16384, E = 32, sigma = 4 (tables read through L2): z and
+        # normalised features of 2 N(0,1) rows against the oracle, which runs
+        # the reference algorithm on the GPU's factors (bit-exact to the
+        # reference's for blocks 0/31, TestFactors.test_config4_factors).
+        import paper_1702_08159_b200 as P
+        meta = json.loads(str(load_npz("c4_blocks.npz")["meta"][0]))
+        spec = _spec(meta)
+        bs = P.build_blocks(spec)
+        ospec = off.OSpec.of(spec)
+        oblocks = [off.OBlock(*bs[e].numpy(), e) for e in range(spec.expansions)]
+        x = synthetic.gaussian_rows(2, 16384, seed=meta["xseed"])
+        want = off.apply_zhat_batch(ospec, oblocks, x)
+        zz = P.apply_zhat_batch(spec, bs, x)
+        assert np.abs(zz - want).max() <= 2e-6 * np.abs(want).max()
+        f = P.feature_map_batch(spec, bs, x)
+        fw = off.feature_map_batch(ospec, oblocks, x)
+        np.testing.assert_allclose(f, fw, rtol=1e-5, atol=1e-6)
+        zp = P.apply_zhat_batch(spec, bs, x, variant="parity")
+        np.testing.assert_array_equal(zp, off.apply_zhat_batch(ospec, oblocks, x, wht="sequential"))
+
     def test_parity_variant_z_bit_exact(self, cuda):
         P, z, spec, x = self._config("c0")
         zz = P.apply_zhat_batch(spec, P.build_blocks(spec), x, variant="parity")

@@ -23,3 +23,15 @@ elif what == "fwht":
         P.wht_fast_batch(buf)
 torch.cuda.synchronize()
 print("done")
+
+if what == "c3":
+    from paper_1702_08159_b200 import synthetic as S
+    x, y = S.class_images(60000, 784, 10, seed=1234)
+    xt, yt = S.class_images(10000, 784, 10, seed=1234, sample_seed=99)
+    spec = P.FeatureMapSpec(784, 8, P.RBF(1.0), 1234)
+    tr = P.Trainer(spec, P.Dataset(x, y, 10), P.Dataset(xt, yt, 10), P.TrainConfig(0.01, 1000, 1))
+    for s in range(5):
+        tr.step(0, s)
+    tr.evaluate()
+    torch.cuda.synchronize()
+    print("c3 done")
