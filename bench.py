@@ -306,6 +306,21 @@ def extras(args, P, torch, dev, hbm):
                            "GBps": round(256 * (65536 + 4 * (1 << 20)) / (ms4 / 1e3) / 1e9, 1),
                            "build_blocks_s": round(setup4, 3)}
     del o4, x4
+    # config 4 fused training step (K6): one rank's 1024-row shard of the
+    # 8192-row global batch; forward + backward (expansion recomputed) + SGD,
+    # features never written to HBM
+    from paper_1702_08159_b200.large_scale import FusedClassifier
+    fc = FusedClassifier(spec4, 10, 1024)
+    x4 = torch.randn((1024, 16384), generator=torch.Generator(device=dev).manual_seed(7),
+                     device=dev)
+    y4 = torch.randint(0, 10, (1024,), device=dev, dtype=torch.int32)
+    fc.step(x4, y4, m_total=8192, lr=0.01)
+    ms_step = time_cuda(lambda: fc.step(x4, y4, m_total=8192, lr=0.01), 3, torch)
+    out["c4_fused_step"] = {"rows_per_rank": 1024, "global_batch": 8192, "ms_per_step": round(ms_step, 3),
+                            "features_per_s": 1024 * (1 << 20) / (ms_step / 1e3),
+                            "note": "forward+backward+update; features_per_s counts each row's 2^20 "
+                                    "features once per step"}
+    del fc, x4
     # config 3: one training epoch (60 steps of 1000 rows + 10k-row evaluation)
     x, y = synthetic.class_images(60000, 784, 10, seed=1234)
     xt, yt = synthetic.class_images(10000, 784, 10, seed=1234, sample_seed=99)

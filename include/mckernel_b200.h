@@ -151,6 +151,32 @@ int mck_head_backward_sgd(const float* phi, int64_t m, int64_t num_features,
                           double* w, double* b, double lr, double l2, void* scratch,
                           void* stream);
 
+/* ----------------- fused expansion -> classifier (BASELINE config 4, K6) */
+/* The softmax head of linear_model.py:95-142 applied to the feature map of
+ * fastfood.py:209-226 (normalize=False) without materialising the features:
+ * z is produced one block at a time into an L2-resident scratch and cos/sin
+ * are formed inside the contraction.  W is float32 (C x 2nE); b, logits,
+ * probs, delta and the loss are float64.  Scratch:
+ * mck_fused_scratch_bytes(m, n, C). */
+int64_t mck_fused_scratch_bytes(int64_t m, int64_t n, int32_t num_classes);
+
+/* logits = phi W^T (+ b inside the softmax), softmax, loss_sum, hits and
+ * delta = (probs - onehot) / m_total, as mck_head_forward.  delta required. */
+int mck_fused_forward(const void* tables, int64_t input_dim, int32_t expansions, double sigma,
+                      const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
+                      const float* w, const double* b, int32_t num_classes,
+                      const int32_t* labels, const int32_t* label_index, int64_t m_total,
+                      double* logits, double* probs, double* delta, double* loss_sum,
+                      int64_t* hits, void* scratch, void* stream);
+
+/* dW = delta^T phi (recomputing phi) and db = sum_r delta_r.  If w != NULL
+ * the SGD update W -= lr*(dW + 2*l2*W), b -= lr*db is applied in place and
+ * dw/db may be NULL; otherwise dW (float32) and db are written. */
+int mck_fused_backward(const void* tables, int64_t input_dim, int32_t expansions, double sigma,
+                       const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
+                       const double* delta, int32_t num_classes, float* dw, double* db,
+                       float* w, double* b, double lr, double l2, void* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,14 @@ int head_backward_sgd(const float*, int64_t, int64_t, int64_t, const double*, in
 int head_sgd_update(double*, double*, const double*, const double*, int64_t, int32_t, double,
                     double, cudaStream_t);
 int64_t head_scratch_bytes(int64_t, int64_t, int32_t);
+int64_t fused_scratch_bytes(int64_t, int64_t, int32_t);
+int fused_forward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
+                  const int32_t*, const float*, const double*, int32_t, const int32_t*,
+                  const int32_t*, int64_t, double*, double*, double*, double*, int64_t*, void*,
+                  cudaStream_t);
+int fused_backward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
+                   const int32_t*, const double*, int32_t, float*, double*, float*, double*,
+                   double, double, void*, cudaStream_t);
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 static int64_t next_pow2(int64_t d) {
@@ -260,6 +268,45 @@ int mck_head_backward_sgd(const float* phi, int64_t m, int64_t F, int64_t ld, co
   if (F < 1 || ld < F) return fail_value("bad feature geometry");
   if (!(lr > 0.0)) return fail_value("learning rate must be positive");
   return head_backward_sgd(phi, m, F, ld, delta, C, w, b, lr, l2, scratch, S(st));
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int64_t mck_fused_scratch_bytes(int64_t m, int64_t n, int32_t C) {
+  if (m < 0 || n < 1 || C < 2) return 0;
+  return fused_scratch_bytes(m, n, C);
+}
+
+int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double sigma,
+                      const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
+                      const float* w, const double* b, int32_t C, const int32_t* labels,
+                      const int32_t* label_index, int64_t m_total, double* logits, double* probs,
+                      double* delta, double* loss_sum, int64_t* hits, void* scratch, void* st) {
+  const int64_t n = next_pow2(input_dim);
+  MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
+  if (m > 0 && (!w || !b || !delta || !scratch)) return fail_value("NULL argument");
+  if (m_total < m) m_total = m;
+  TablesView tv;
+  tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
+  return fused_forward(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, w, b, C, labels,
+                       label_index, m_total, logits, probs, delta, loss_sum, hits, scratch, S(st));
+}
+
+int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double sigma,
+                       const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
+                       const double* delta, int32_t C, float* dw, double* db, float* w, double* b,
+                       double lr, double l2, void* scratch, void* st) {
+  const int64_t n = next_pow2(input_dim);
+  MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
+  if (m > 0 && (!delta || !scratch)) return fail_value("NULL argument");
+  if (w && !(lr > 0.0)) return fail_value("learning rate must be positive");
+  if (!w && !dw) return fail_value("either w (fused update) or dw is required");
+  TablesView tv;
+  tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
+  return fused_backward(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, delta, C, dw, db, w,
+                        b, lr, l2, scratch, S(st));
 }
 
 }  // extern "C"

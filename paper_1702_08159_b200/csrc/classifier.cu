@@ -374,4 +374,22 @@ int head_sgd_update(double* w, double* b, const double* dw, const double* db, in
 
 int64_t head_scratch_bytes(int64_t m, int64_t F, int32_t C) { return head_layout(m, F, C, nullptr, nullptr); }
 
+// Softmax / loss / delta / hits from finished logits (without bias), used by
+// the fused config-4 path (fused_head.cu).
+int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const double* b,
+                             const int32_t* labels, const int32_t* label_index, int64_t m_total,
+                             double* probs, double* delta, double* loss_sum, int64_t* hits,
+                             double* rowloss, int32_t* rowhit, cudaStream_t st) {
+  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  if (m == 0) return MCK_OK;
+  k_head_softmax<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+      logits, 1, m, C, b, labels, label_index, m_total, probs, delta, rowloss, rowhit);
+  MCK_TRY(check_launch("k_head_softmax"));
+  if (labels && (loss_sum || hits)) {
+    k_head_reduce<<<1, 1024, 0, st>>>(rowloss, rowhit, m, loss_sum, hits);
+    MCK_TRY(check_launch("k_head_reduce"));
+  }
+  return MCK_OK;
+}
+
 }  // namespace mck

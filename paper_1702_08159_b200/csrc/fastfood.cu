@@ -128,8 +128,9 @@ struct FFParams {
   float norm;
   float* out;
   int64_t ldo;
-  int32_t E;
+  int32_t E;   // blocks computed: e0 .. e0+E-1, written at columns (e-e0)*n
   int64_t D;
+  int32_t e0;
 };
 
 // Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
@@ -158,7 +159,7 @@ k_fastfood(FFParams p) {
   const int64_t total_it = my_groups * p.E;
 
   auto issue = [&](int64_t it) {  // thread 0 only
-    const int e = (int)(it % p.E);
+    const int e = p.e0 + (int)(it % p.E);
     unsigned char* dst = tabs + (it & 1) * SLOT;
     uint64_t* b = bar + (it & 1);
     mbar_expect_tx(b, tab_bytes<C>());
@@ -213,9 +214,9 @@ k_fastfood(FFParams p) {
         t_cs = reinterpret_cast<const float*>(tb + N * 8);
         t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
       } else {
-        t_scat = p.scat + (int64_t)e * N;
-        t_cs = p.cs + (int64_t)e * N;
-        t_bm = p.bmask + (int64_t)e * bm_stride<C>();
+        t_scat = p.scat + (int64_t)(p.e0 + e) * N;
+        t_cs = p.cs + (int64_t)(p.e0 + e) * N;
+        t_bm = p.bmask + (int64_t)(p.e0 + e) * bm_stride<C>();
       }
 
       float v[R];
@@ -417,6 +418,8 @@ int launch_ff_cfg(const FFParams& p, bool feat, bool fold, bool vec, cudaStream_
   return vec ? launch_ff<C, false, false, true>(p, st) : launch_ff<C, false, false, false>(p, st);
 }
 
+int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream_t st);
+
 int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                  int64_t ldx, const int32_t* rows, bool feat, bool normalize, float* out,
                  int64_t ldo, int variant, cudaStream_t st) {
@@ -454,8 +457,34 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
   p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
   p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs;
   p.scale = scale; p.norm = norm; p.out = out; p.ldo = ldo; p.E = tv.E; p.D = D;
-  const bool vec = (d % 4 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  if ((ldo % 4) || (reinterpret_cast<uintptr_t>(out) & 15))
+  return launch_by_logn(p, logn, feat, fold, st);
+}
+
+// z of blocks e0 .. e0+ecount-1 only (columns 0 .. ecount*n of z): the
+// producer half of the fused config-4 path (fused_head.cu).
+int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                      int64_t ldx, const int32_t* rows, int32_t e0, int32_t ecount, float* z,
+                      int64_t ldz, cudaStream_t st) {
+  if (m == 0) return MCK_OK;
+  const int64_t n = tv.n;
+  const float scale = (float)(1.0 / (sigma * sqrt((double)n)));
+  int ex = 0;
+  const bool fold = frexpf(scale, &ex) == 0.5f;
+  int logn = 0;
+  while ((int64_t(1) << logn) < n) ++logn;
+  if (logn < 3 || logn > 14) return fail_value("fused path supports padded_dim 8..16384");
+  if (e0 < 0 || ecount < 1 || e0 + ecount > tv.E) return fail_value("block range out of bounds");
+  FFParams p{};
+  p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
+  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs;
+  p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
+  p.e0 = e0;
+  return launch_by_logn(p, logn, false, fold, st);
+}
+
+int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream_t st) {
+  const bool vec = (p.d % 4 == 0) && (p.ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
+  if ((p.ldo % 4) || (reinterpret_cast<uintptr_t>(p.out) & 15))
     return fail_value("output rows must be 16-byte aligned");
   switch (logn) {
     case 3: return launch_ff_cfg<RowCfg<3, 2>>(p, feat, fold, vec, st);
@@ -470,7 +499,7 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
     case 12: return launch_ff_cfg<RowCfg<12, 5>>(p, feat, fold, vec, st);
     case 13: return launch_ff_cfg<RowCfg<13, 5>>(p, feat, fold, vec, st);
     case 14: return launch_ff_cfg<RowCfg<14, 5>>(p, feat, fold, vec, st);
-    default: return fail_value("unsupported padded_dim %lld", (long long)n);
+    default: return fail_value("unsupported padded_dim 2^%d", logn);
   }
 }
 

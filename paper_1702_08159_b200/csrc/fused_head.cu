@@ -1,0 +1,328 @@
+// K6 -- fused expansion -> softmax classifier for the largest configuration
+// (BASELINE config 4: d = n = 16384, E = 32, 2^20 features per row, 10
+// classes).  Features are never written to HBM:
+//
+//   for each block e:   k_fastfood (z of block e only, fastfood_z_blocks)
+//                         -> z tile (m x n fp32) in an L2-resident scratch
+//                       k_fused_fwd: cos/sin computed on the fly from z,
+//                         contracted with the W slice of block e (shared
+//                         memory) into per-chunk partial logits
+//                       k_fused_fold: partial logits -> float64 logits
+//                         (fixed order: blocks ascending, chunks ascending)
+//   softmax / loss / delta (classifier.cu, k_head_softmax)
+//   for each block e:   k_fastfood again (recompute z; cheaper than storing
+//                         2^20 features per row)
+//                       k_fused_bwd: dW slice of block e = delta^T [cos z | sin z]
+//                         with cos/sin on the fly, row-split partials
+//                       k_fused_dw_finish: reduce splits (fixed order) and
+//                         either write dW (multi-GPU: all-reduced by the
+//                         caller) or apply the SGD update in place.
+//
+// W is float32 (C x 2nE; 41.9 MB at config 4, the all-reduce payload named in
+// SURVEY.md section 2.1), logits and loss float64, contraction accumulators
+// float32 within a chunk of 512 features.
+#include <type_traits>
+
+#include "mck_common.cuh"
+#include "tables.cuh"
+
+namespace mck {
+
+int fastfood_z_blocks(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
+                      const int32_t*, int32_t, int32_t, float*, int64_t, cudaStream_t);
+int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const double* b,
+                             const int32_t* labels, const int32_t* label_index, int64_t m_total,
+                             double* probs, double* delta, double* loss_sum, int64_t* hits,
+                             double* rowloss, int32_t* rowhit, cudaStream_t st);
+
+constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
+constexpr int kFwarps = 8;
+constexpr int kFrowsPerWarp = 4;
+constexpr int kFrows = kFwarps * kFrowsPerWarp;
+constexpr int kBzPerThread = 4;
+constexpr int kBthreads = 256;
+constexpr int kBz = kBzPerThread * kBthreads;  // z values per backward CTA
+constexpr int kBrowChunk = 128;
+constexpr int kFusedMaxClasses = 16;
+
+struct FusedScratch {
+  float* z;          // [m][n]
+  float* lpart;      // [KS][m][C]     partial logits of the current block
+  double* logits;    // [m][C]
+  double* rowloss;   // [m]
+  int32_t* rowhit;   // [m]
+  double* delta64;   // [m][C]
+  float* delta32;    // [m][C]
+  float* dwpart;     // [RS][C][2n]    backward partials of the current block
+};
+
+inline int64_t fused_rsplits(int64_t m) {
+  int64_t rs = (m + 63) / 64;
+  return rs > 16 ? 16 : (rs < 1 ? 1 : rs);
+}
+
+inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedScratch* fs) {
+  auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += al(bytes);
+    return p;
+  };
+  const int64_t KS = (n + kFzChunk - 1) / kFzChunk;
+  FusedScratch s{};
+  s.z = (float*)take(m * n * 4);
+  s.lpart = (float*)take(KS * m * C * 4);
+  s.logits = (double*)take(m * C * 8);
+  s.rowloss = (double*)take(m * 8);
+  s.rowhit = (int32_t*)take(m * 4);
+  s.delta64 = (double*)take(m * C * 8);
+  s.delta32 = (float*)take(m * C * 4);
+  s.dwpart = (float*)take(fused_rsplits(m) * C * 2 * n * 4);
+  if (fs) *fs = s;
+  return off;
+}
+
+// lpart[ks][r][c] = sum_{i in chunk ks} cos(z[r][i]) W[c][e n + i] + sin(z[r][i]) W[c][D + e n + i]
+template <int NC>
+__global__ void __launch_bounds__(kFwarps * 32) k_fused_fwd(const float* __restrict__ z, int64_t m,
+                                                            int64_t n, const float* __restrict__ w,
+                                                            int64_t F, int64_t col_cos,
+                                                            int64_t col_sin, float* __restrict__ lpart) {
+  __shared__ __align__(16) float wc[NC][kFzChunk];
+  __shared__ __align__(16) float wsn[NC][kFzChunk];
+  const int ks = blockIdx.y;
+  const int64_t i0 = (int64_t)ks * kFzChunk;
+  const int ni = (int)(n - i0 < kFzChunk ? n - i0 : kFzChunk);
+  for (int t = threadIdx.x; t < NC * kFzChunk; t += blockDim.x) {
+    const int c = t / kFzChunk, i = t % kFzChunk;
+    wc[c][i] = i < ni ? w[(int64_t)c * F + col_cos + i0 + i] : 0.f;
+    wsn[c][i] = i < ni ? w[(int64_t)c * F + col_sin + i0 + i] : 0.f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * kFrows + warp * kFrowsPerWarp;
+  float acc[kFrowsPerWarp][NC];
+#pragma unroll
+  for (int q = 0; q < kFrowsPerWarp; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[q][c] = 0.f;
+  const float* zr[kFrowsPerWarp];
+#pragma unroll
+  for (int q = 0; q < kFrowsPerWarp; ++q) zr[q] = z + (r0 + q < m ? r0 + q : m - 1) * n + i0;
+  for (int i = lane; i < ni; i += 32) {
+    float cs[kFrowsPerWarp], sn[kFrowsPerWarp];
+#pragma unroll
+    for (int q = 0; q < kFrowsPerWarp; ++q) __sincosf(__ldg(zr[q] + i), &sn[q], &cs[q]);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const float a = wc[c][i], b = wsn[c][i];
+#pragma unroll
+      for (int q = 0; q < kFrowsPerWarp; ++q) acc[q][c] = fmaf(cs[q], a, fmaf(sn[q], b, acc[q][c]));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kFrowsPerWarp; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      float v = acc[q][c];
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      acc[q][c] = v;
+    }
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < kFrowsPerWarp; ++q)
+      if (r0 + q < m)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) lpart[((int64_t)ks * m + r0 + q) * NC + c] = acc[q][c];
+}
+
+// logits[r][c] (+)= sum_ks lpart[ks][r][c]   (float64, chunk order)
+__global__ void k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C,
+                             double* logits, int first) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m * C) return;
+  double s = first ? 0.0 : logits[t];
+  for (int64_t k = 0; k < KS; ++k) s += (double)lpart[k * m * C + t];
+  logits[t] = s;
+}
+
+__global__ void k_to_f32(const double* a, float* b, int64_t n) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) b[t] = (float)a[t];
+}
+
+// dwpart[rs][c][i]      = sum_{r in split} delta[r][c] cos(z[r][i])
+// dwpart[rs][c][n + i]  = sum_{r in split} delta[r][c] sin(z[r][i])
+template <int NC>
+__global__ void __launch_bounds__(kBthreads) k_fused_bwd(const float* __restrict__ z, int64_t m,
+                                                         int64_t n, const float* __restrict__ delta,
+                                                         int64_t rows_per_split,
+                                                         float* __restrict__ dwpart) {
+  __shared__ float sd[kBrowChunk][NC];
+  const int rs = blockIdx.y;
+  const int64_t rbeg = (int64_t)rs * rows_per_split;
+  const int64_t rend = rbeg + rows_per_split < m ? rbeg + rows_per_split : m;
+  const int64_t ib = (int64_t)blockIdx.x * kBz + threadIdx.x;
+  float ac[kBzPerThread][NC], as[kBzPerThread][NC];
+#pragma unroll
+  for (int j = 0; j < kBzPerThread; ++j)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) ac[j][c] = as[j][c] = 0.f;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kBrowChunk) {
+    const int nr = (int)(rend - r0 < kBrowChunk ? rend - r0 : kBrowChunk);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nr * NC; t += blockDim.x) sd[t / NC][t % NC] = delta[r0 * NC + t];
+    __syncthreads();
+#pragma unroll 2
+    for (int rr = 0; rr < nr; ++rr) {
+      const float* zr = z + (r0 + rr) * n;
+      float cs[kBzPerThread], sn[kBzPerThread];
+#pragma unroll
+      for (int j = 0; j < kBzPerThread; ++j) {
+        const int64_t i = ib + j * kBthreads;
+        const float zz = i < n ? __ldg(zr + i) : 0.f;
+        __sincosf(zz, &sn[j], &cs[j]);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const float d = sd[rr][c];
+#pragma unroll
+        for (int j = 0; j < kBzPerThread; ++j) {
+          ac[j][c] = fmaf(d, cs[j], ac[j][c]);
+          as[j][c] = fmaf(d, sn[j], as[j][c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kBzPerThread; ++j) {
+    const int64_t i = ib + j * kBthreads;
+    if (i < n)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        dwpart[((int64_t)rs * NC + c) * 2 * n + i] = ac[j][c];
+        dwpart[((int64_t)rs * NC + c) * 2 * n + n + i] = as[j][c];
+      }
+  }
+}
+
+// For block e: g = sum_rs dwpart (fixed order); dw[c][col] = g, or
+// w[c][col] -= lr*(g + 2*l2*w) in place.  col = e n + i (cos) / D + e n + i (sin).
+__global__ void k_fused_dw_finish(const float* __restrict__ dwpart, int64_t RS, int C, int64_t n,
+                                  int64_t F, int64_t col_cos, int64_t col_sin, float* dw, float* w,
+                                  float lr, float l2) {
+  const int64_t per = 2 * n;
+  const int64_t total = (int64_t)C * per;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = t / per, k = t % per;
+    float g = 0.f;
+    for (int64_t s = 0; s < RS; ++s) g += dwpart[s * total + t];
+    const int64_t col = c * F + (k < n ? col_cos + k : col_sin + (k - n));
+    if (w) {
+      const float wv = w[col];
+      w[col] = wv - lr * (l2 != 0.f ? g + 2.f * l2 * wv : g);
+    } else {
+      dw[col] = g;
+    }
+  }
+}
+
+__global__ void k_fused_db(const double* delta, int64_t m, int C, double* db, double* b, double lr) {
+  __shared__ double s[256];
+  const int c = blockIdx.x;
+  double a = 0.0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) a += delta[r * C + c];
+  s[threadIdx.x] = a;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (db) db[c] = s[0];
+    if (b) b[c] -= lr * s[0];
+  }
+}
+
+template <class Fn>
+static int dispatch_nc(int C, Fn fn) {
+  switch (C) {
+#define MCK_D(N) case N: return fn(std::integral_constant<int, N>{});
+    MCK_D(2) MCK_D(3) MCK_D(4) MCK_D(5) MCK_D(6) MCK_D(7) MCK_D(8) MCK_D(9) MCK_D(10)
+    MCK_D(11) MCK_D(12) MCK_D(13) MCK_D(14) MCK_D(15) MCK_D(16)
+#undef MCK_D
+    default: return fail_value("num_classes must be in 2..%d", kFusedMaxClasses);
+  }
+}
+
+int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t C) { return fused_layout(m, n, C, nullptr, nullptr); }
+
+int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                  int64_t ldx, const int32_t* rows, const float* w, const double* b, int32_t C,
+                  const int32_t* labels, const int32_t* label_index, int64_t m_total,
+                  double* logits_out, double* probs, double* delta, double* loss_sum,
+                  int64_t* hits, void* scratch, cudaStream_t st) {
+  if (m == 0) return MCK_OK;
+  const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
+  FusedScratch fs;
+  fused_layout(m, n, C, (char*)scratch, &fs);
+  const int64_t KS = (n + kFzChunk - 1) / kFzChunk;
+  for (int32_t e = 0; e < E; ++e) {
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
+    MCK_TRY(dispatch_nc(C, [&](auto nc) {
+      constexpr int NC = decltype(nc)::value;
+      dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
+      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(fs.z, m, n, w, F, (int64_t)e * n,
+                                                     D + (int64_t)e * n, fs.lpart);
+      return check_launch("k_fused_fwd");
+    }));
+    k_fused_fold<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(fs.lpart, KS, m, C, fs.logits,
+                                                                  e == 0 ? 1 : 0);
+    MCK_TRY(check_launch("k_fused_fold"));
+  }
+  if (logits_out)
+    MCK_TRY(check_cuda(cudaMemcpyAsync(logits_out, fs.logits, m * C * 8, cudaMemcpyDeviceToDevice, st),
+                       "logits copy"));
+  return head_softmax_from_logits(fs.logits, m, C, b, labels, label_index, m_total, probs,
+                                  delta ? delta : fs.delta64, loss_sum, hits, fs.rowloss,
+                                  fs.rowhit, st);
+}
+
+int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                   int64_t ldx, const int32_t* rows, const double* delta, int32_t C, float* dw,
+                   double* db, float* w, double* b, double lr, double l2, void* scratch,
+                   cudaStream_t st) {
+  if (m == 0) return MCK_OK;
+  const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
+  FusedScratch fs;
+  fused_layout(m, n, C, (char*)scratch, &fs);
+  const int64_t RS = fused_rsplits(m);
+  const int64_t rps = (m + RS - 1) / RS;
+  k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
+  MCK_TRY(check_launch("k_to_f32"));
+  for (int32_t e = 0; e < E; ++e) {
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
+    MCK_TRY(dispatch_nc(C, [&](auto nc) {
+      constexpr int NC = decltype(nc)::value;
+      dim3 grid((unsigned)((n + kBz - 1) / kBz), (unsigned)RS);
+      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(fs.z, m, n, fs.delta32, rps, fs.dwpart);
+      return check_launch("k_fused_bwd");
+    }));
+    int64_t grid = ((int64_t)C * 2 * n + 255) / 256;
+    if (grid > 148 * 8) grid = 148 * 8;
+    k_fused_dw_finish<<<(unsigned)grid, 256, 0, st>>>(fs.dwpart, RS, C, n, F, (int64_t)e * n,
+                                                      D + (int64_t)e * n, dw, w, (float)lr,
+                                                      (float)l2);
+    MCK_TRY(check_launch("k_fused_dw_finish"));
+  }
+  k_fused_db<<<C, 256, 0, st>>>(delta, m, C, db, b, lr);
+  return check_launch("k_fused_db");
+}
+
+}  // namespace mck

@@ -1,0 +1,83 @@
+"""K6 (config 4): fused expansion -> classifier against the materialised path.
+
+The materialised path is the parity-tested expansion (test_gpu_parity.py)
+followed by the same softmax arithmetic in float64 (linear_model.py:95-131):
+logits = phi W^T, delta = (softmax(logits + b) - onehot)/m, dW = delta^T phi.
+Tolerances: the fused contraction accumulates in float32 within 512-feature
+chunks and in float64 across chunks -> logits within 1e-5 of max|logits|,
+dW within 1e-4 of max|dW|.
+"""
+
+import numpy as np
+import pytest
+
+from paper_1702_08159_b200 import synthetic
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(cuda, spec, m, seed):
+    import paper_1702_08159_b200 as P
+    from paper_1702_08159_b200.large_scale import FusedClassifier
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    if spec.input_dim == 784:
+        x = torch.from_numpy(synthetic.image_rows(m, 784, seed)).cuda()
+    else:
+        x = torch.randn((m, spec.input_dim), generator=g, device="cuda")
+    y = torch.randint(0, 10, (m,), generator=g, device="cuda", dtype=torch.int32)
+    fc = FusedClassifier(spec, 10, m)
+    fc.w.copy_(torch.randn(fc.w.shape, generator=g, device="cuda") * 0.01)
+    fc.b.copy_(torch.randn(10, generator=g, device="cuda", dtype=torch.float64) * 0.1)
+    phi = P.feature_map_batch(spec, fc.blocks, x, normalize=False).double()
+    return fc, x, y, phi
+
+
+@pytest.mark.parametrize("which", ["small", "c4"])
+def test_fused_forward_backward(cuda, which):
+    import paper_1702_08159_b200 as P
+    torch = cuda
+    if which == "small":
+        spec, m = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3), 96
+    else:
+        spec, m = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4), 8
+    fc, x, y, phi = _case(cuda, spec, m, 11)
+    logits = torch.empty((m, 10), dtype=torch.float64, device="cuda")
+    probs = torch.empty((m, 10), dtype=torch.float64, device="cuda")
+    fc.forward(x, y, logits=logits, probs=probs)
+    want = phi @ fc.w.double().T
+    err = (logits - want).abs().max().item()
+    assert err <= 1e-5 * want.abs().max().item(), err
+    p = torch.softmax(want + fc.b, dim=1)
+    assert (probs - p).abs().max().item() <= 1e-6
+    loss = -torch.log(p[torch.arange(m), y.long()]).sum().item()
+    assert abs(fc.loss_sum.item() - loss) <= 1e-5 * abs(loss)
+    delta = p.clone()
+    delta[torch.arange(m), y.long()] -= 1.0
+    delta /= m
+    assert (fc.delta[:m] - delta).abs().max().item() <= 1e-7
+    dw = fc.backward(x, m).double()
+    dw_ref = delta.T @ phi
+    assert (dw - dw_ref).abs().max().item() <= 1e-4 * dw_ref.abs().max().item()
+    assert torch.allclose(fc.db64, fc.delta[:m].sum(0), rtol=1e-12, atol=1e-15)
+    assert torch.allclose(fc.db64, delta.sum(0), rtol=1e-5, atol=1e-8)
+
+
+def test_fused_sgd_update_and_gather(cuda):
+    import paper_1702_08159_b200 as P
+    torch = cuda
+    spec = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3)
+    fc, x, y, phi = _case(cuda, spec, 128, 5)
+    rows = torch.tensor(list(range(0, 128, 2)), dtype=torch.int32, device="cuda")
+    w0, b0 = fc.w.clone(), fc.b.clone()
+    fc.forward(x, y, rows=rows, m_total=64)
+    ph = phi[rows.long()]
+    p = torch.softmax(ph @ w0.double().T + b0, dim=1)
+    d = p.clone()
+    d[torch.arange(64), y[rows.long()].long()] -= 1.0
+    d /= 64
+    assert (fc.delta[:64] - d).abs().max().item() <= 1e-7
+    fc.backward(x, 64, rows=rows, lr=0.5)
+    w_ref = w0.double() - 0.5 * (d.T @ ph)
+    assert (fc.w.double() - w_ref).abs().max().item() <= 1e-6
+    assert torch.allclose(fc.b, b0 - 0.5 * d.sum(0), rtol=1e-6, atol=1e-9)
