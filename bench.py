@@ -52,48 +52,50 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clock and throttle reasons via NVML while the timed region runs."""
+    """Samples SM clock and throttle reasons during the timed region with a
+    separate `nvidia-smi -lms` process (no GIL contention with the launches)."""
 
-    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-             0x100: "display_clock_setting"}
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.samples, self.reasons = [], 0
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
+    def __init__(self, index: int, interval_ms: int = 20):
+        self.index, self.interval = index, interval_ms
+        self.proc, self.lines = None, []
 
     def __enter__(self):
+        import subprocess
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-
-            def loop():
-                while not self._stop.is_set():
-                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                    self.reasons |= int(pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
-                    time.sleep(0.005)
-
-            self._t = threading.Thread(target=loop, daemon=True)
-            self._t.start()
-        except Exception as exc:  # NVML unavailable: report it
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", str(self.interval)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample before the timed region starts
+        except OSError as exc:
             self.error = str(exc)
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+        if self.proc:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        reasons = [n for bit, n in self.NAMES.items() if self.reasons & bit and n != "gpu_idle"]
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": reasons}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            f = [x.strip() for x in line.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------------ distributed
@@ -199,7 +201,7 @@ def bench_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "kernel": "k_fastfood<RowCfg<10,5>,FEAT,FOLD=0,VEC>",
+                "kernel": "k_fastfood<RowCfg<10,5>,FEAT=1,FOLD=1,VEC=1> (scale 1/64 folded into C)",
                 "alg_bytes_per_launch": int(batch * bytes_per_row),
                 "avg_launch_us": round(tot_ms / (args.steps * len(spans)) * 1e3, 2)}
 
@@ -418,7 +420,7 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-rows", type=int, default=4096)

@@ -35,3 +35,14 @@ if what == "c3":
     tr.evaluate()
     torch.cuda.synchronize()
     print("c3 done")
+
+if what == "c4":
+    from paper_1702_08159_b200.large_scale import FusedClassifier
+    spec = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4)
+    fc = FusedClassifier(spec, 10, 1024)
+    x = torch.randn((1024, 16384), device="cuda")
+    y = torch.randint(0, 10, (1024,), device="cuda", dtype=torch.int32)
+    fc.step(x, y, m_total=8192, lr=0.01)
+    fc.step(x, y, m_total=8192, lr=0.01)
+    torch.cuda.synchronize()
+    print("c4 done")
