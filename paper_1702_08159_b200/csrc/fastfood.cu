@@ -255,18 +255,22 @@ k_fastfood(FFParams p) {
         const float4 c4 = *reinterpret_cast<const float4*>(t_cs + i0);
         float z[4] = {v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]};
         const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) z[c] = FOLD ? z[c] * cc[c] : (z[c] * cc[c]) * p.scale;
+        mul_pk(z[0], z[1], cc[0], cc[1]);
+        mul_pk(z[2], z[3], cc[2], cc[3]);
+        if constexpr (!FOLD) {
+          mul_pk(z[0], z[1], p.scale, p.scale);
+          mul_pk(z[2], z[3], p.scale, p.scale);
+        }
         if (valid) {
           float* o = orow + (int64_t)e * N + i0;
           if constexpr (FEAT) {
             float sn[4], cn[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              sincos_fast(z[c], sn[c], cn[c]);
-              sn[c] *= p.norm;
-              cn[c] *= p.norm;
-            }
+            for (int c = 0; c < 4; ++c) sincos_fast(z[c], sn[c], cn[c]);
+            mul_pk(sn[0], sn[1], p.norm, p.norm);
+            mul_pk(sn[2], sn[3], p.norm, p.norm);
+            mul_pk(cn[0], cn[1], p.norm, p.norm);
+            mul_pk(cn[2], cn[3], p.norm, p.norm);
             *reinterpret_cast<float4*>(o) = make_float4(cn[0], cn[1], cn[2], cn[3]);
             *reinterpret_cast<float4*>(o + p.D) = make_float4(sn[0], sn[1], sn[2], sn[3]);
           } else {

@@ -101,15 +101,44 @@ __device__ __forceinline__ uint32_t thread_part(uint32_t tid) {
   return deposit_bits(tid, FULL & ~P);
 }
 
+// Packed fp32 pair butterfly (a0,a1) <- (a0,a1)+(b0,b1), (b0,b1) <- (a0,a1)-(b0,b1):
+// sm_100 FADD2 does two lanes' worth of adds per instruction.
+__device__ __forceinline__ void bfly_pk(float& a0, float& a1, float& b0, float& b1) {
+  unsigned long long A, B, S, D;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(S) : "l"(A), "l"(B));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(D) : "l"(A), "l"(B));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a0), "=f"(a1) : "l"(S));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(b0), "=f"(b1) : "l"(D));
+}
+
+// (a0,a1) *= (b0,b1) with one FMUL2.
+__device__ __forceinline__ void mul_pk(float& a0, float& a1, float b0, float b1) {
+  unsigned long long A, B, M;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(A) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(B) : "f"(b0), "f"(b1));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(M) : "l"(A), "l"(B));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(a0), "=f"(a1) : "l"(M));
+}
+
 // Butterflies over the register-index bits whose deposited index bit is in
-// ACTIVE (a subset of P).
+// ACTIVE (a subset of P).  For fp32, stages on register bits >= 1 combine
+// register pairs (2m, 2m+1) with packed FADD2; the stage on register bit 0
+// (inside a pair) stays scalar.
 template <int R, uint32_t P, uint32_t ACTIVE, class V>
 __device__ __forceinline__ void butterflies(V (&v)[R]) {
 #pragma unroll
   for (int a = 0; (1 << a) < R; ++a) {
-    constexpr int dummy = 0;
-    (void)dummy;
     if (ACTIVE & deposit_bits(1u << a, P)) {
+      if constexpr (sizeof(V) == 4) {
+        if (a >= 1) {
+#pragma unroll
+          for (int k = 0; k < R; k += 2)
+            if (!(k & (1 << a))) bfly_pk(v[k], v[k + 1], v[k | (1 << a)], v[(k | (1 << a)) + 1]);
+          continue;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         if (!(k & (1 << a))) {
