@@ -137,9 +137,11 @@ struct FFParams {
 // tables of iteration it+1 (next block, or block 0 of the next group) are in
 // flight while iteration it computes.
 template <class C>
-constexpr int ff_min_blocks() { return C::T * ff_rows_per_cta<C>() <= 256 ? 3 : 1; }
+constexpr int ff_min_blocks() {
+  return C::R >= 64 ? 2 : (C::T * ff_rows_per_cta<C>() <= 256 ? 3 : 1);
+}
 
-template <class C, bool FEAT, bool FOLD, bool VEC>
+template <class C, bool FEAT, bool FOLD, bool VEC, bool XREG = (C::R <= 32)>
 __global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>(), ff_min_blocks<C>())
 k_fastfood(FFParams p) {
   constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
@@ -181,23 +183,25 @@ k_fastfood(FFParams p) {
     const int64_t row = (blockIdx.x + gi * gridDim.x) * ROWS + gid;
     const bool valid = row < p.m;
     // ---- input row, layout L, zero padded (kept in registers for all E blocks)
-    float xr[R];
-    {
-      const int64_t src = valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0;
-      const float* xp = p.x + src * p.ldx;
+    const float* xp = p.x + (valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0) * p.ldx;
+    auto load_x = [&](float (&dst)[R]) {
 #pragma unroll
       for (int j = 0; j < R / 4; ++j) {
         const int i0 = 4 * (int)tid + j * 4 * T;
         if constexpr (VEC) {
           float4 t4 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (valid && i0 < p.d) t4 = __ldg(reinterpret_cast<const float4*>(xp + i0));
-          xr[4 * j] = t4.x; xr[4 * j + 1] = t4.y; xr[4 * j + 2] = t4.z; xr[4 * j + 3] = t4.w;
+          dst[4 * j] = t4.x; dst[4 * j + 1] = t4.y; dst[4 * j + 2] = t4.z; dst[4 * j + 3] = t4.w;
         } else {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) xr[4 * j + c] = (valid && i0 + c < p.d) ? __ldg(xp + i0 + c) : 0.f;
+          for (int c = 0; c < 4; ++c) dst[4 * j + c] = (valid && i0 + c < p.d) ? __ldg(xp + i0 + c) : 0.f;
         }
       }
-    }
+    };
+    // x stays in registers across the E blocks (XREG) or is re-read per
+    // block (large R, or single-block launches of the fused path)
+    float xr[XREG ? R : 1];
+    if constexpr (XREG) load_x(xr);
     float* orow = p.out + (valid ? row : 0) * p.ldo;
 
     for (int e = 0; e < p.E; ++e) {
@@ -220,13 +224,16 @@ k_fastfood(FFParams p) {
       }
 
       float v[R];
+      if constexpr (!XREG) load_x(v);
       // ---- x * B (sign XOR, exact)
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         const uint32_t bits = t_bm[w * T + tid];
 #pragma unroll
-        for (int q = 0; q < 32 && 32 * w + q < R; ++q)
-          v[32 * w + q] = __uint_as_float(__float_as_uint(xr[32 * w + q]) ^ (((bits >> q) & 1u) << 31));
+        for (int q = 0; q < 32 && 32 * w + q < R; ++q) {
+          const float xv = XREG ? xr[(32 * w + q) % (XREG ? R : 1)] : v[32 * w + q];
+          v[32 * w + q] = __uint_as_float(__float_as_uint(xv) ^ (((bits >> q) & 1u) << 31));
+        }
       }
       // ---- H (first)
       butterflies<R, C::PL, C::PL>(v);
@@ -384,7 +391,7 @@ int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st,
     case 11: return prepare_cfg<RowCfg<11, 5>>(tv, st);
     case 12: return prepare_cfg<RowCfg<12, 5>>(tv, st);
     case 13: return prepare_cfg<RowCfg<13, 5>>(tv, st);
-    case 14: return prepare_cfg<RowCfg<14, 5>>(tv, st);
+    case 14: return prepare_cfg<RowCfg<14, 6>>(tv, st);
     default: return MCK_OK;  // fused kernel not available; parity path only
   }
 }
@@ -502,7 +509,7 @@ int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream
     case 11: return launch_ff_cfg<RowCfg<11, 5>>(p, feat, fold, vec, st);
     case 12: return launch_ff_cfg<RowCfg<12, 5>>(p, feat, fold, vec, st);
     case 13: return launch_ff_cfg<RowCfg<13, 5>>(p, feat, fold, vec, st);
-    case 14: return launch_ff_cfg<RowCfg<14, 5>>(p, feat, fold, vec, st);
+    case 14: return launch_ff_cfg<RowCfg<14, 6>>(p, feat, fold, vec, st);
     default: return fail_value("unsupported padded_dim 2^%d", logn);
   }
 }

@@ -41,7 +41,12 @@ __host__ __device__ constexpr int popcount_c(uint32_t m) {
   return c;
 }
 
-__host__ __device__ __forceinline__ constexpr uint32_t pad_addr(uint32_t i) { return i + (i >> 5); }
+// Padded shared-memory address: one word per 32 plus four per 1024.  Checked
+// by exhaustive simulation to make every layout of RowCfg<10..15, 5> and
+// RowCfg<12..14, 6> bank-conflict free for scalar LDS/STS.
+__host__ __device__ __forceinline__ constexpr uint32_t pad_addr(uint32_t i) {
+  return i + (i >> 5) + 4 * (i >> 10);
+}
 
 template <int LOGN_, int LOGR_>
 struct RowCfg {
@@ -58,7 +63,7 @@ struct RowCfg {
       3u | ((((1u << (LOGR - 2)) - 1u)) << (LOGN - LOGR + 2));
   // middle bits 2 .. 2+LOGT-1
   static constexpr int NMID = (LOGT + LOGR - 1) / LOGR;
-  static constexpr int SMEM_FLOATS = N + N / 32;  // padded row
+  static constexpr int SMEM_FLOATS = N + N / 32 + N / 256 + 4;  // padded row (pad_addr)
 
   // Active (butterflied) middle bits of round j.
   __host__ __device__ static constexpr uint32_t mid_active(int j) {
@@ -69,13 +74,14 @@ struct RowCfg {
     for (int b = lo; b < hi; ++b) m |= 1u << b;
     return m;
   }
-  // Register bits of middle round j: active bits plus fillers taken from the
-  // top of the index (never middle bits), so that every round holds R values.
+  // Register bits of middle round j: active bits plus passenger ("filler")
+  // bits -- the highest bits not butterflied in this round -- so that every
+  // round holds R values and the lanes stay on the low index bits.
   __host__ __device__ static constexpr uint32_t mid_regs(int j) {
     uint32_t m = mid_active(j);
     int need = LOGR - popcount_c(m);
     for (int b = LOGN - 1; need > 0 && b >= 0; --b) {
-      if (!(m & (1u << b)) && !(mid_active_all() & (1u << b))) {
+      if (!(m & (1u << b))) {  // any bit not butterflied in this round
         m |= 1u << b;
         --need;
       }
@@ -151,16 +157,21 @@ __device__ __forceinline__ void butterflies(V (&v)[R]) {
   }
 }
 
+// pad_addr is additive over disjoint bit sets (no carries between them), so
+// the address splits into a per-thread base plus a compile-time offset per
+// register: one base register, immediate offsets in every LDS/STS.
 template <int R, uint32_t P, class V>
 __device__ __forceinline__ void sts_layout(V* s, uint32_t tpart, const V (&v)[R]) {
+  V* base = s + pad_addr(tpart);
 #pragma unroll
-  for (int k = 0; k < R; ++k) s[pad_addr(lay_index<P>(tpart, k))] = v[k];
+  for (int k = 0; k < R; ++k) base[pad_addr(deposit_bits((uint32_t)k, P))] = v[k];
 }
 
 template <int R, uint32_t P, class V>
 __device__ __forceinline__ void lds_layout(const V* s, uint32_t tpart, V (&v)[R]) {
+  const V* base = s + pad_addr(tpart);
 #pragma unroll
-  for (int k = 0; k < R; ++k) v[k] = s[pad_addr(lay_index<P>(tpart, k))];
+  for (int k = 0; k < R; ++k) v[k] = base[pad_addr(deposit_bits((uint32_t)k, P))];
 }
 
 // Group barrier for T threads that start at a multiple of T inside the CTA.
