@@ -304,3 +304,44 @@ def param_count(spec: FeatureMapSpec, num_classes: int) -> int:
     if num_classes < 2:
         raise ValueError("need at least two classes")
     return num_classes * (feature_dim(spec) + 1)
+
+
+# -- plain-text spec config (checkpoints) -----------------------------------
+
+def spec_to_config(spec: FeatureMapSpec) -> str:
+    """key=value text used inside MCKMODL1 checkpoints (fastfood.py:264-274)."""
+    lines = [
+        f"d={spec.input_dim}",
+        f"E={spec.expansions}",
+        f"kernel={'rbf' if isinstance(spec.kernel, RBF) else 'matern'}",
+        f"sigma={spec.kernel.sigma!r}",
+        f"t={spec.kernel.t if isinstance(spec.kernel, RBFMatern) else 0}",
+        f"seed={spec.seed}",
+    ]
+    return "\n".join(lines) + "\n"
+
+
+def spec_from_config(text: str) -> FeatureMapSpec:
+    """Inverse of :func:`spec_to_config` (fastfood.py:277-300)."""
+    fields: dict[str, str] = {}
+    for line in text.strip().splitlines():
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        key, _, value = line.partition("=")
+        fields[key.strip()] = value.strip()
+    try:
+        d = int(fields["d"])
+        expansions = int(fields["E"])
+        kind = fields["kernel"]
+        sigma = float(fields["sigma"])
+        seed = int(fields["seed"])
+    except KeyError as exc:
+        raise ValueError(f"config is missing key {exc}") from exc
+    if kind == "rbf":
+        kernel: Kernel = RBF(sigma)
+    elif kind == "matern":
+        kernel = RBFMatern(sigma, int(fields.get("t", "0")))
+    else:
+        raise ValueError(f"unknown kernel kind {kind!r}")
+    return FeatureMapSpec(input_dim=d, expansions=expansions, kernel=kernel, seed=seed)

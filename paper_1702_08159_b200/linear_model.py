@@ -371,3 +371,43 @@ def evaluate(model: SoftmaxModel, spec, ds, *, chunk: int = 4096):
         head.forward(phi, m, model, labels=y[s0:s0 + m], delta=False,
                      loss_sum=ls.data_ptr() + 8 * k, hits=hs.data_ptr() + 8 * k)
     return int(hs.sum().item()) / n, float(ls.sum().item()) / n
+
+
+# -- checkpoints (MCKMODL1, linear_model.py:248-272) ------------------------
+
+MODEL_MAGIC = b"MCKMODL1"
+
+
+def save_model(path, model: SoftmaxModel, spec) -> None:
+    """Magic, spec text, then W and b float64 records -- readable by the reference's load_model."""
+    from . import dataio
+    config = fastfood.spec_to_config(spec) if spec is not None else "kernel=none\n"
+    payload = config.encode("utf-8")
+    w, b = model.numpy()
+    with open(path, "wb") as f:
+        f.write(MODEL_MAGIC)
+        f.write(len(payload).to_bytes(4, "little"))
+        f.write(payload)
+        dataio.write_matrix_record(f, np.ascontiguousarray(w, dtype=np.float64))
+        dataio.write_matrix_record(f, np.ascontiguousarray(b, dtype=np.float64)[None, :])
+
+
+def read_model_arrays(path):
+    """(W, b, spec) from an MCKMODL1 file, host-side (no GPU needed)."""
+    from . import dataio
+    with open(path, "rb") as f:
+        magic = f.read(8)
+        if magic != MODEL_MAGIC:
+            raise ValueError(f"{path}: not a model checkpoint (magic {magic!r})")
+        size = int.from_bytes(f.read(4), "little")
+        config = f.read(size).decode("utf-8")
+        w = dataio.read_matrix_record(f)
+        b = dataio.read_matrix_record(f)[0]
+    spec = None if "kernel=none" in config else fastfood.spec_from_config(config)
+    return w, b, spec
+
+
+def load_model(path, device=None):
+    """Inverse of :func:`save_model`; the model is placed on the GPU."""
+    w, b, spec = read_model_arrays(path)
+    return SoftmaxModel(w, b, device), spec

@@ -92,3 +92,68 @@ def wht_fast_batch(mat, base_size: int = DEFAULT_BASE_SIZE, *, variant: str = "f
     if mat.ndim != 2:
         raise ValueError("wht_fast_batch expects an (m, n) array")
     return _transform(mat, base_size, variant)
+
+
+# -- benchmark (wht.py:165-205; paper Table 1) -------------------------------
+
+from dataclasses import dataclass  # noqa: E402
+
+
+@dataclass
+class BenchRecord:
+    size: int
+    fast_ms: float
+    naive_ms: float | None
+    reps: int
+
+
+def bench_wht(sizes, repetitions: int = 5, naive_cutoff: int = 1 << 16, dtype=np.float32):
+    """Median device time per single-vector transform (CUDA events), Table-1 style.
+
+    ``fast_ms`` times ``mck_fwht_f32`` on one resident vector of each size
+    (the reference times ``wht_fast`` on the host, wht.py:183-205).
+    ``naive_ms`` times the O(n^2) product with the dense +-1 matrix on the
+    GPU (float32 matmul) up to ``naive_cutoff``, as the reference's oracle.
+    """
+    if repetitions < 3:
+        raise ValueError("repetitions must be at least 3")
+    for s in sizes:
+        _check_pow2(s)
+    torch = nat.require_cuda()
+    rng = np.random.default_rng(0)
+    recs = []
+    for size in sizes:
+        proto = torch.from_numpy(rng.standard_normal(size).astype(dtype)).cuda()
+
+        def med(fn):
+            times = []
+            for _ in range(repetitions):
+                buf = proto.clone()
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                fn(buf)
+                e.record()
+                e.synchronize()
+                times.append(s.elapsed_time(e))
+            return float(np.median(times))
+
+        wht_fast(proto.clone())                     # warm-up
+        fast = med(wht_fast)
+        naive = None
+        if size <= naive_cutoff and size <= 1 << 13:
+            h = torch.ones((1, 1), dtype=proto.dtype, device="cuda")
+            while h.shape[0] < size:                # Sylvester: H_2n = [[H, H], [H, -H]]
+                h = torch.cat([torch.cat([h, h], 1), torch.cat([h, -h], 1)], 0)
+            naive = med(lambda b: h @ b)
+        recs.append(BenchRecord(size, fast, naive, repetitions))
+    return recs
+
+
+def bench_wht_csv(records) -> str:
+    """CSV ``size,impl,median_ms,reps`` exactly as ``mckernel bench-wht`` (cli.py:115-132)."""
+    lines = ["size,impl,median_ms,reps"]
+    for r in records:
+        lines.append(f"{r.size},fast,{r.fast_ms:.6f},{r.reps}")
+        if r.naive_ms is not None:
+            lines.append(f"{r.size},naive,{r.naive_ms:.6f},{r.reps}")
+    return "\n".join(lines) + "\n"

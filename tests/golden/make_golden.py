@@ -186,6 +186,17 @@ def gen_train(name, c):
              w_norm=float(np.sqrt((model.w ** 2).sum())), b=model.b.tolist()), indent=1))
 
 
+def gen_formats():
+    """Byte-level fixtures of the reference's on-disk formats."""
+    from mckernel import dataio as rdio
+    spec = rf.FeatureMapSpec(5, 2, rf.RBFMatern(1.5, 3), 77)
+    m = rl.SoftmaxModel(np.arange(3 * 20, dtype=np.float64).reshape(3, 20) / 7.0,
+                        np.array([0.5, -1.25, 3.0]))
+    rl.save_model(HERE / "model_small.mckmodl", m, spec)
+    rdio.write_matrix(HERE / "matrix_small.mckmat",
+                      (np.arange(12, dtype=np.float32).reshape(3, 4) - 5) / 3)
+
+
 JOBS = {
     "detrand": gen_detrand,
     "blocks_small": gen_blocks_small,
@@ -196,6 +207,7 @@ JOBS = {
     "train_c3h": lambda: gen_train("train_c3h", C3H),
     "train_c3": lambda: gen_train("train_c3", C3),
     "train_tiny": lambda: gen_train("train_tiny", TINY),
+    "formats": gen_formats,
 }
 
 if __name__ == "__main__":
@@ -206,3 +218,4 @@ if __name__ == "__main__":
         t0 = time.time()
         JOBS[name]()
         print(f"{name}: {time.time() - t0:.1f}s", flush=True)
+

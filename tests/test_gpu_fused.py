@@ -81,3 +81,42 @@ def test_fused_sgd_update_and_gather(cuda):
     w_ref = w0.double() - 0.5 * (d.T @ ph)
     assert (fc.w.double() - w_ref).abs().max().item() <= 1e-6
     assert torch.allclose(fc.b, b0 - 0.5 * d.sum(0), rtol=1e-6, atol=1e-9)
+
+
+def test_kernel_check_bench_wht_and_feature_dump(cuda, tmp_path):
+    # next-ranked items of SURVEY.md section 8f, on the GPU path
+    import paper_1702_08159_b200 as P
+    from paper_1702_08159_b200 import dataio
+    from paper_1702_08159_b200.exact_kernel import kernel_check
+    from paper_1702_08159_b200.wht import bench_wht, bench_wht_csv
+    rng = np.random.default_rng(7)
+    spec = P.FeatureMapSpec(64, 8, P.RBF(1.0), 31)
+    pairs = [(rng.standard_normal(64) * 0.3, rng.standard_normal(64) * 0.3) for _ in range(100)]
+    st = kernel_check(spec, pairs)
+    assert st.D == 512 and st.pairs == 100 and st.mean_err <= 0.05      # test_fastfood.py:247-258
+    recs = bench_wht([1024, 4096, 1 << 20], repetitions=3)
+    csv = bench_wht_csv(recs).splitlines()
+    assert csv[0] == "size,impl,median_ms,reps" and len(csv) == 1 + 3 + 2
+    assert all(r.fast_ms > 0 for r in recs) and recs[2].naive_ms is None
+    x = synthetic.image_rows(300, 784, 3)
+    spec2 = P.FeatureMapSpec(784, 2, P.RBF(1.0), 9)
+    bs = P.build_blocks(spec2)
+    path = tmp_path / "f.mckmat"
+    assert dataio.features_to_file(spec2, bs, x, path, batch_rows=128) == (300, 4096)
+    got = dataio.read_matrix(path)
+    np.testing.assert_array_equal(got, P.feature_map_batch(spec2, bs, x))
+
+
+def test_checkpoint_round_trip_gpu(cuda, tmp_path):
+    import paper_1702_08159_b200 as P
+    from paper_1702_08159_b200.linear_model import load_model, save_model
+    spec = P.FeatureMapSpec(20, 2, P.RBF(1.0), 5)
+    m = P.SoftmaxModel(np.random.default_rng(0).standard_normal((10, 128)), np.arange(10.0))
+    save_model(tmp_path / "m", m, spec)
+    m2, spec2 = load_model(tmp_path / "m")
+    assert spec2 == spec
+    assert torch_equal(m2.w, m.w) and torch_equal(m2.b, m.b)
+
+
+def torch_equal(a, b):
+    return bool((a == b).all().item())
