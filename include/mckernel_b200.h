@@ -161,13 +161,15 @@ int mck_head_backward_sgd(const float* phi, int64_t m, int64_t num_features,
 int64_t mck_fused_scratch_bytes(int64_t m, int64_t n, int32_t num_classes);
 
 /* logits = phi W^T (+ b inside the softmax), softmax, loss_sum, hits and
- * delta = (probs - onehot) / m_total, as mck_head_forward.  delta required. */
+ * delta = (probs - onehot) / m_total, as mck_head_forward.  delta required.
+ * variant 0: contraction on the tensor cores (tcgen05 kind::tf32, 3xTF32 split,
+ * TMEM accumulators); variant 1: CUDA-core fp32 FMA (cross-check). */
 int mck_fused_forward(const void* tables, int64_t input_dim, int32_t expansions, double sigma,
                       const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
                       const float* w, const double* b, int32_t num_classes,
                       const int32_t* labels, const int32_t* label_index, int64_t m_total,
                       double* logits, double* probs, double* delta, double* loss_sum,
-                      int64_t* hits, void* scratch, void* stream);
+                      int64_t* hits, void* scratch, int32_t variant, void* stream);
 
 /* dW = delta^T phi (recomputing phi) and db = sum_r delta_r.  If w != NULL
  * the SGD update W -= lr*(dW + 2*l2*W), b -= lr*db is applied in place and
@@ -175,7 +177,13 @@ int mck_fused_forward(const void* tables, int64_t input_dim, int32_t expansions,
 int mck_fused_backward(const void* tables, int64_t input_dim, int32_t expansions, double sigma,
                        const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
                        const double* delta, int32_t num_classes, float* dw, double* db,
-                       float* w, double* b, double lr, double l2, void* scratch, void* stream);
+                       float* w, double* b, double lr, double l2, void* scratch,
+                       int32_t variant, void* stream);
+
+/* -------------------------------------------------------------- diagnostics */
+/* tcgen05 self-test: D (128 x 16) = A (128 x K) * B (16 x K)^T, kind::tf32,
+ * operands via shared memory, accumulator in TMEM (K % 8 == 0, K <= 256). */
+int mck_diag_umma_tf32(const float* A, const float* B, float* D, int32_t K, void* stream);
 
 #ifdef __cplusplus
 }

@@ -65,10 +65,10 @@ int64_t fused_scratch_bytes(int64_t, int64_t, int32_t);
 int fused_forward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
                   const int32_t*, const float*, const double*, int32_t, const int32_t*,
                   const int32_t*, int64_t, double*, double*, double*, double*, int64_t*, void*,
-                  cudaStream_t);
+                  int32_t, cudaStream_t);
 int fused_backward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
                    const int32_t*, const double*, int32_t, float*, double*, float*, double*,
-                   double, double, void*, cudaStream_t);
+                   double, double, void*, int32_t, cudaStream_t);
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 static int64_t next_pow2(int64_t d) {
@@ -283,7 +283,8 @@ int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double s
                       const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
                       const float* w, const double* b, int32_t C, const int32_t* labels,
                       const int32_t* label_index, int64_t m_total, double* logits, double* probs,
-                      double* delta, double* loss_sum, int64_t* hits, void* scratch, void* st) {
+                      double* delta, double* loss_sum, int64_t* hits, void* scratch,
+                      int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
   if (m > 0 && (!w || !b || !delta || !scratch)) return fail_value("NULL argument");
@@ -291,13 +292,14 @@ int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double s
   TablesView tv;
   tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
   return fused_forward(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, w, b, C, labels,
-                       label_index, m_total, logits, probs, delta, loss_sum, hits, scratch, S(st));
+                       label_index, m_total, logits, probs, delta, loss_sum, hits, scratch,
+                       variant, S(st));
 }
 
 int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double sigma,
                        const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
                        const double* delta, int32_t C, float* dw, double* db, float* w, double* b,
-                       double lr, double l2, void* scratch, void* st) {
+                       double lr, double l2, void* scratch, int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
   if (m > 0 && (!delta || !scratch)) return fail_value("NULL argument");
@@ -306,7 +308,7 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double 
   TablesView tv;
   tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
   return fused_backward(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, delta, C, dw, db, w,
-                        b, lr, l2, scratch, S(st));
+                        b, lr, l2, scratch, variant, S(st));
 }
 
 }  // extern "C"

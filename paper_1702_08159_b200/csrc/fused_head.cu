@@ -36,6 +36,7 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
                              double* rowloss, int32_t* rowhit, cudaStream_t st);
 
 constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
+int64_t fused_tc_ksplits(int64_t n);  // fused_tc.cu
 constexpr int kFwarps = 8;
 constexpr int kFrowsPerWarp = 4;
 constexpr int kFrows = kFwarps * kFrowsPerWarp;
@@ -69,7 +70,8 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
     off += al(bytes);
     return p;
   };
-  const int64_t KS = (n + kFzChunk - 1) / kFzChunk;
+  const int64_t KS_cc = (n + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(n);
+  const int64_t KS = KS_cc > KS_tc ? KS_cc : KS_tc;   // partial-logit chunks of either variant
   FusedScratch s{};
   s.z = (float*)take(m * n * 4);
   s.lpart = (float*)take(KS * m * C * 4);
@@ -263,19 +265,27 @@ static int dispatch_nc(int C, Fn fn) {
 
 int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t C) { return fused_layout(m, n, C, nullptr, nullptr); }
 
+int fused_fwd_tc(const float*, int64_t, int64_t, const float*, int64_t, int, int64_t, int64_t,
+                 float*, cudaStream_t);
+int fused_bwd_tc(const float*, int64_t, int64_t, const float*, int, int64_t, int64_t, int64_t,
+                 float*, float*, float, float, cudaStream_t);
+int64_t fused_tc_ksplits(int64_t n);
+
 int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                   int64_t ldx, const int32_t* rows, const float* w, const double* b, int32_t C,
                   const int32_t* labels, const int32_t* label_index, int64_t m_total,
                   double* logits_out, double* probs, double* delta, double* loss_sum,
-                  int64_t* hits, void* scratch, cudaStream_t st) {
+                  int64_t* hits, void* scratch, int32_t cuda_cores, cudaStream_t st) {
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;
   fused_layout(m, n, C, (char*)scratch, &fs);
-  const int64_t KS = (n + kFzChunk - 1) / kFzChunk;
+  const int64_t KS = cuda_cores ? (n + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(n);
   for (int32_t e = 0; e < E; ++e) {
     MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
-    MCK_TRY(dispatch_nc(C, [&](auto nc) {
+    if (!cuda_cores)
+      MCK_TRY(fused_fwd_tc(fs.z, m, n, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+    else MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
       k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(fs.z, m, n, w, F, (int64_t)e * n,
@@ -297,7 +307,7 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
 int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                    int64_t ldx, const int32_t* rows, const double* delta, int32_t C, float* dw,
                    double* db, float* w, double* b, double lr, double l2, void* scratch,
-                   cudaStream_t st) {
+                   int32_t cuda_cores, cudaStream_t st) {
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;
@@ -308,6 +318,11 @@ int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x
   MCK_TRY(check_launch("k_to_f32"));
   for (int32_t e = 0; e < E; ++e) {
     MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
+    if (!cuda_cores) {
+      MCK_TRY(fused_bwd_tc(fs.z, m, n, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw, w,
+                           (float)lr, (float)l2, st));
+      continue;
+    }
     MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((n + kBz - 1) / kBz), (unsigned)RS);

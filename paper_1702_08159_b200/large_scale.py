@@ -20,7 +20,8 @@ from .distributed import world
 class FusedClassifier:
     """Softmax head (W float32 C x 2nE, b float64) over fused Fastfood features."""
 
-    def __init__(self, spec, num_classes: int, max_rows: int, device=None):
+    def __init__(self, spec, num_classes: int, max_rows: int, device=None, *,
+                 tensor_cores: bool = True):
         torch = nat.require_cuda()
         if num_classes < 2:
             raise ValueError("need at least two classes")
@@ -39,6 +40,7 @@ class FusedClassifier:
         self.hits = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.rank, self.ws = world()
         self.dw = None
+        self.variant = 0 if tensor_cores else 1   # tcgen05 contraction / CUDA-core cross-check
 
     def _x(self, x):
         torch = nat.require_cuda()
@@ -62,7 +64,7 @@ class FusedClassifier:
                  m_total or m, nat.ptr(logits), nat.ptr(probs), nat.ptr(self.delta),
                  nat.ptr(self.loss_sum) if labels is not None else None,
                  nat.ptr(self.hits) if labels is not None else None, nat.ptr(self.scratch),
-                 nat.stream_handle(self.dev))
+                 self.variant, nat.stream_handle(self.dev))
         return m
 
     def backward(self, x, m, rows=None, lr=None, l2=0.0):
@@ -76,7 +78,7 @@ class FusedClassifier:
                 nat.ptr(self.delta), self.C)
         if lr is not None and self.ws == 1:
             nat.call("mck_fused_backward", *args, None, None, nat.ptr(self.w), nat.ptr(self.b),
-                     float(lr), float(l2), nat.ptr(self.scratch), st)
+                     float(lr), float(l2), nat.ptr(self.scratch), self.variant, st)
             return None
         if self.dw is None:
             # flat [dW (f32, C*F) | db (f32 copy, C) | loss_sum | hits] for one all-reduce
@@ -84,7 +86,7 @@ class FusedClassifier:
             self.dw = self.flat[:self.C * self.F].view(self.C, self.F)
             self.db64 = torch.zeros(self.C, dtype=torch.float64, device=self.dev)
         nat.call("mck_fused_backward", *args, nat.ptr(self.dw), nat.ptr(self.db64), None, None,
-                 0.0, 0.0, nat.ptr(self.scratch), st)
+                 0.0, 0.0, nat.ptr(self.scratch), self.variant, st)
         return self.dw
 
     def step(self, x, labels, rows=None, m_total=None, lr=0.01, l2=0.0):

@@ -16,7 +16,7 @@ from paper_1702_08159_b200 import synthetic
 pytestmark = pytest.mark.gpu
 
 
-def _case(cuda, spec, m, seed):
+def _case(cuda, spec, m, seed, tc=True):
     import paper_1702_08159_b200 as P
     from paper_1702_08159_b200.large_scale import FusedClassifier
     torch = cuda
@@ -26,22 +26,23 @@ def _case(cuda, spec, m, seed):
     else:
         x = torch.randn((m, spec.input_dim), generator=g, device="cuda")
     y = torch.randint(0, 10, (m,), generator=g, device="cuda", dtype=torch.int32)
-    fc = FusedClassifier(spec, 10, m)
+    fc = FusedClassifier(spec, 10, m, tensor_cores=tc)
     fc.w.copy_(torch.randn(fc.w.shape, generator=g, device="cuda") * 0.01)
     fc.b.copy_(torch.randn(10, generator=g, device="cuda", dtype=torch.float64) * 0.1)
     phi = P.feature_map_batch(spec, fc.blocks, x, normalize=False).double()
     return fc, x, y, phi
 
 
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
 @pytest.mark.parametrize("which", ["small", "c4"])
-def test_fused_forward_backward(cuda, which):
+def test_fused_forward_backward(cuda, which, tc):
     import paper_1702_08159_b200 as P
     torch = cuda
     if which == "small":
         spec, m = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3), 96
     else:
         spec, m = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4), 8
-    fc, x, y, phi = _case(cuda, spec, m, 11)
+    fc, x, y, phi = _case(cuda, spec, m, 11, tc)
     logits = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     probs = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     fc.forward(x, y, logits=logits, probs=probs)
@@ -49,25 +50,27 @@ def test_fused_forward_backward(cuda, which):
     err = (logits - want).abs().max().item()
     assert err <= 1e-5 * want.abs().max().item(), err
     p = torch.softmax(want + fc.b, dim=1)
-    assert (probs - p).abs().max().item() <= 1e-6
+    # |dp| <= max|d logits| (softmax is 1-Lipschitz in the max norm up to a factor 1/2)
+    assert (probs - p).abs().max().item() <= max(1e-6, 1.0 * err)
     loss = -torch.log(p[torch.arange(m), y.long()]).sum().item()
     assert abs(fc.loss_sum.item() - loss) <= 1e-5 * abs(loss)
     delta = p.clone()
     delta[torch.arange(m), y.long()] -= 1.0
     delta /= m
-    assert (fc.delta[:m] - delta).abs().max().item() <= 1e-7
+    assert (fc.delta[:m] - delta).abs().max().item() <= max(1e-7, err / m)
     dw = fc.backward(x, m).double()
     dw_ref = delta.T @ phi
     assert (dw - dw_ref).abs().max().item() <= 1e-4 * dw_ref.abs().max().item()
     assert torch.allclose(fc.db64, fc.delta[:m].sum(0), rtol=1e-12, atol=1e-15)
-    assert torch.allclose(fc.db64, delta.sum(0), rtol=1e-5, atol=1e-8)
+    assert torch.allclose(fc.db64, delta.sum(0), rtol=1e-5, atol=max(1e-8, err))
 
 
-def test_fused_sgd_update_and_gather(cuda):
+@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
+def test_fused_sgd_update_and_gather(cuda, tc):
     import paper_1702_08159_b200 as P
     torch = cuda
     spec = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3)
-    fc, x, y, phi = _case(cuda, spec, 128, 5)
+    fc, x, y, phi = _case(cuda, spec, 128, 5, tc)
     rows = torch.tensor(list(range(0, 128, 2)), dtype=torch.int32, device="cuda")
     w0, b0 = fc.w.clone(), fc.b.clone()
     fc.forward(x, y, rows=rows, m_total=64)
