@@ -96,7 +96,8 @@ __global__ void k_prepare(const float* b, const float* g, const int32_t* perminv
     const int64_t off = e * (int64_t)C::N;
     const uint32_t j = lay_index<PM>(thread_part<C::FULL, PM>(tid), k);
     const int32_t pinv = perminv[off + j];
-    scat[t] = make_uint2(pad_addr((uint32_t)pinv), __float_as_uint(g[off + pinv]));
+    // byte offset into the row's shared buffer: STS [offset + uniform base]
+    scat[t] = make_uint2(4u * pad_addr((uint32_t)pinv), __float_as_uint(g[off + pinv]));
     if (k < W) {
       uint32_t bits = 0;
       for (int q = 0; q < 32 && 32 * k + q < R; ++q) {
@@ -247,7 +248,9 @@ k_fastfood(FFParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + tid];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s[a[q].x] = v[k0 + q] * __uint_as_float(a[q].y);
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float*>(reinterpret_cast<char*>(s) + a[q].x) =
+              v[k0 + q] * __uint_as_float(a[q].y);
       }
       group_sync<T>(gid);
       lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
@@ -255,11 +258,15 @@ k_fastfood(FFParams p) {
       // ---- H (second), ending in layout L
       middle_rounds_then_L<C, 0, R>(s, tid, gid, v);
       butterflies<R, C::PL, C::PL>(v);
-      // ---- C * scale, feature epilogue
+      // ---- C * scale, feature epilogue.  Output pointers are formed once per
+      // block (per-j offsets are compile-time), the math runs unconditionally
+      // and only the stores are predicated on the row being valid.
+      float* const ob = orow + (int64_t)e * N + 4 * (int)tid;
+      float* const obs = ob + p.D;
+      const float* const csb = t_cs + 4 * (int)tid;
 #pragma unroll
       for (int j = 0; j < R / 4; ++j) {
-        const int i0 = 4 * (int)tid + j * 4 * T;
-        const float4 c4 = *reinterpret_cast<const float4*>(t_cs + i0);
+        const float4 c4 = *reinterpret_cast<const float4*>(csb + j * 4 * T);
         float z[4] = {v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]};
         const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
         mul_pk(z[0], z[1], cc[0], cc[1]);
@@ -268,21 +275,20 @@ k_fastfood(FFParams p) {
           mul_pk(z[0], z[1], p.scale, p.scale);
           mul_pk(z[2], z[3], p.scale, p.scale);
         }
-        if (valid) {
-          float* o = orow + (int64_t)e * N + i0;
-          if constexpr (FEAT) {
-            float sn[4], cn[4];
+        if constexpr (FEAT) {
+          float sn[4], cn[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) sincos_fast(z[c], sn[c], cn[c]);
-            mul_pk(sn[0], sn[1], p.norm, p.norm);
-            mul_pk(sn[2], sn[3], p.norm, p.norm);
-            mul_pk(cn[0], cn[1], p.norm, p.norm);
-            mul_pk(cn[2], cn[3], p.norm, p.norm);
-            *reinterpret_cast<float4*>(o) = make_float4(cn[0], cn[1], cn[2], cn[3]);
-            *reinterpret_cast<float4*>(o + p.D) = make_float4(sn[0], sn[1], sn[2], sn[3]);
-          } else {
-            *reinterpret_cast<float4*>(o) = make_float4(z[0], z[1], z[2], z[3]);
+          for (int c = 0; c < 4; ++c) sincos_fast(z[c], sn[c], cn[c]);
+          mul_pk(sn[0], sn[1], p.norm, p.norm);
+          mul_pk(sn[2], sn[3], p.norm, p.norm);
+          mul_pk(cn[0], cn[1], p.norm, p.norm);
+          mul_pk(cn[2], cn[3], p.norm, p.norm);
+          if (valid) {
+            *reinterpret_cast<float4*>(ob + j * 4 * T) = make_float4(cn[0], cn[1], cn[2], cn[3]);
+            *reinterpret_cast<float4*>(obs + j * 4 * T) = make_float4(sn[0], sn[1], sn[2], sn[3]);
           }
+        } else {
+          if (valid) *reinterpret_cast<float4*>(ob + j * 4 * T) = make_float4(z[0], z[1], z[2], z[3]);
         }
       }
     }
