@@ -185,6 +185,12 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t expansions
  * operands via shared memory, accumulator in TMEM (K % 8 == 0, K <= 256). */
 int mck_diag_umma_tf32(const float* A, const float* B, float* D, int32_t K, void* stream);
 
+/* Host-only (no GPU): the proper 32-edge-colouring used to lay out the
+ * permutation Pi (fastfood.py:192) in shared memory without bank conflicts.
+ * Edge e joins left node l[e] to right node r[e] (m nodes per side, every node
+ * of degree 32); col[e] in [0, 32).  Returns 0, or 1 if not 32-regular. */
+int mck_diag_edge_color32(int32_t m, const int32_t* l, const int32_t* r, uint8_t* col);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,9 +6,10 @@
 // in registers for all E blocks.  Per block:
 //   x*B  : sign-bit XOR from a per-thread mask word          (fastfood.py:190)
 //   H    : register butterflies + shared-memory exchanges     (:191)
-//   Pi,G : one scatter into shared memory: z1[j] goes to perm^-1[j] already
-//          multiplied by g[perm^-1[j]] (the same fp32 product the reference
-//          forms after its gather, :192-193)
+//   Pi,G : one scatter into shared memory: z1[j] goes to perm^-1[j]'s slot
+//          already multiplied by g[perm^-1[j]] (the same fp32 product the
+//          reference forms after its gather, :192-193); slots are edge-
+//          coloured so scatter and gather are bank-conflict free
 //   H    : middle rounds first, ending in the 16-byte store layout (:194)
 //   C*s  : one multiply when 1/(sigma*sqrt n) is a power of two (exactly the
 //          reference's two roundings), else two               (:195-196)
@@ -22,6 +23,9 @@
 #include "fwht_core.cuh"
 #include "tables.cuh"
 #include "async_copy.cuh"
+#include "perm_color.cuh"
+
+#include <vector>
 
 namespace mck {
 
@@ -29,11 +33,18 @@ template <class C>
 constexpr int ff_rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
 
 // Per-block factor tables, staged into shared memory by TMA bulk copies:
-// scat [R][T] uint2 | cs [N] f32 | bmask [bm_stride] u32.
+// scat [R][T] uint2 | cs [N] f32 | bmask [bm_stride] u32 | gcol [R/4][T] u32.
+// n >= 1024 (whole warps per row) use the edge-coloured permutation
+// (perm_color.cu): scatter and gather are both bank-conflict free; smaller n
+// scatter to the padded layout and gather with the structured layout read.
+template <class C>
+constexpr bool ff_colored() { return C::T >= 32; }
 template <class C>
 constexpr int bm_stride() { return ((((C::R + 31) / 32) * C::T) + 3) & ~3; }
 template <class C>
-constexpr int tab_bytes() { return C::N * 8 + C::N * 4 + bm_stride<C>() * 4; }
+constexpr int tab_bytes() {
+  return C::N * 8 + C::N * 4 + bm_stride<C>() * 4 + (ff_colored<C>() ? C::N : 0);
+}
 template <class C>
 constexpr int tab_slot() { return (tab_bytes<C>() + 127) & ~127; }
 template <class C>
@@ -125,6 +136,7 @@ struct FFParams {
   const uint32_t* bmask;
   const uint2* scat;
   const float* cs;
+  const uint32_t* gcol;
   float scale;
   float norm;
   float* out;
@@ -169,6 +181,8 @@ k_fastfood(FFParams p) {
     bulk_g2s(dst, p.scat + (int64_t)e * N, N * 8, b);
     bulk_g2s(dst + N * 8, p.cs + (int64_t)e * N, N * 4, b);
     bulk_g2s(dst + N * 12, p.bmask + (int64_t)e * bm_stride<C>(), bm_stride<C>() * 4, b);
+    if constexpr (ff_colored<C>())
+      bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)e * (N / 4), N, b);
   };
   if (STAGED) {
     if (threadIdx.x == 0) {
@@ -210,6 +224,7 @@ k_fastfood(FFParams p) {
       const uint2* t_scat;
       const float* t_cs;
       const uint32_t* t_bm;
+      const uint32_t* t_gc;
       if constexpr (STAGED) {
         __syncthreads();  // buffer (it+1)&1 (read at it-1) is free
         if (threadIdx.x == 0 && it + 1 < total_it) issue(it + 1);
@@ -218,10 +233,12 @@ k_fastfood(FFParams p) {
         t_scat = reinterpret_cast<const uint2*>(tb);
         t_cs = reinterpret_cast<const float*>(tb + N * 8);
         t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
+        t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
       } else {
         t_scat = p.scat + (int64_t)(p.e0 + e) * N;
         t_cs = p.cs + (int64_t)(p.e0 + e) * N;
         t_bm = p.bmask + (int64_t)(p.e0 + e) * bm_stride<C>();
+        t_gc = p.gcol + (int64_t)(p.e0 + e) * (N / 4);
       }
 
       float v[R];
@@ -253,7 +270,19 @@ k_fastfood(FFParams p) {
               v[k0 + q] * __uint_as_float(a[q].y);
       }
       group_sync<T>(gid);
-      lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
+      if constexpr (ff_colored<C>()) {
+        // gather group (warp w, register k) occupies words 32*(w*R + k) + colour
+        const char* gb = reinterpret_cast<const char*>(s) + (tid / 32) * (R * 128);
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; ++k4) {
+          const uint32_t cw = t_gc[k4 * T + tid];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v[4 * k4 + q] = *reinterpret_cast<const float*>(gb + (4 * k4 + q) * 128 + ((cw >> (8 * q)) & 0xffu));
+        }
+      } else {
+        lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
+      }
       group_sync<T>(gid);
       // ---- H (second), ending in layout L
       middle_rounds_then_L<C, 0, R>(s, tid, gid, v);
@@ -356,6 +385,60 @@ __global__ void k_fastfood_parity(const float* x, int64_t ldx, int32_t d, const 
   }
 }
 
+// ---------------------------------------------------------------- coloured Pi
+// Host side (one-time setup): slots of the edge-coloured permutation.  H1
+// leaves y[j] in (thread t, register k) of layout PM -> scatter group
+// S = (t/32)*R + k; position p = perm^-1[j] is read by (t', k') of layout P0
+// -> gather group G = (t'/32)*R + k'.  Slot = 32*G + colour(j).
+template <class C>
+int color_tables(const TablesView& tv, cudaStream_t st) {
+  constexpr int R = C::R, T = C::T, N = C::N, M = N / 32;
+  constexpr uint32_t PM = last_mid_regs<C>(), P0 = C::mid_regs(0);
+  const int E = tv.E;
+  std::vector<int32_t> pinv((size_t)E * N);
+  std::vector<uint32_t> gbits((size_t)E * N);
+  MCK_TRY(check_cuda(cudaMemcpyAsync(pinv.data(), tv.perminv, pinv.size() * 4,
+                                     cudaMemcpyDeviceToHost, st), "perminv D2H"));
+  MCK_TRY(check_cuda(cudaMemcpyAsync(gbits.data(), tv.g, gbits.size() * 4,
+                                     cudaMemcpyDeviceToHost, st), "g D2H"));
+  MCK_TRY(check_cuda(cudaStreamSynchronize(st), "colour tables sync"));
+  std::vector<int32_t> sgrp(N), spos(N), ggrp(N), gpos(N);
+  for (int t = 0; t < T; ++t)
+    for (int k = 0; k < R; ++k) {
+      const uint32_t j = deposit_bits((uint32_t)t, C::FULL & ~PM) | deposit_bits((uint32_t)k, PM);
+      sgrp[j] = (t / 32) * R + k;
+      spos[j] = k * T + t;
+      const uint32_t p = deposit_bits((uint32_t)t, C::FULL & ~P0) | deposit_bits((uint32_t)k, P0);
+      ggrp[p] = (t / 32) * R + k;
+      gpos[p] = k * T + t;
+    }
+  std::vector<uint2> scat((size_t)E * N);
+  std::vector<uint32_t> gcol((size_t)E * N / 4, 0u);
+  std::vector<int32_t> left(N), right(N);
+  std::vector<uint8_t> col(N);
+  for (int e = 0; e < E; ++e) {
+    const int32_t* pi = pinv.data() + (size_t)e * N;
+    for (int j = 0; j < N; ++j) {
+      left[j] = sgrp[j];
+      right[j] = ggrp[pi[j]];
+    }
+    if (!edge_color32(M, N, left.data(), right.data(), col.data()))
+      return fail_value("internal: permutation edge colouring failed (block %d)", e);
+    for (int j = 0; j < N; ++j) {
+      const int32_t p = pi[j];
+      scat[(size_t)e * N + spos[j]] =
+          make_uint2(4u * (32u * (uint32_t)ggrp[p] + col[j]), gbits[(size_t)e * N + p]);
+      const int k = gpos[p] / T, t = gpos[p] % T;
+      gcol[(size_t)e * (N / 4) + (k / 4) * T + t] |= (4u * col[j]) << (8 * (k % 4));
+    }
+  }
+  MCK_TRY(check_cuda(cudaMemcpyAsync(tv.scat, scat.data(), scat.size() * 8,
+                                     cudaMemcpyHostToDevice, st), "scat H2D"));
+  MCK_TRY(check_cuda(cudaMemcpyAsync(tv.gcol, gcol.data(), gcol.size() * 4,
+                                     cudaMemcpyHostToDevice, st), "gcol H2D"));
+  return check_cuda(cudaStreamSynchronize(st), "colour tables upload");
+}
+
 // ---------------------------------------------------------------- dispatch
 template <class C>
 int prepare_cfg(const TablesView& tv, cudaStream_t st) {
@@ -363,7 +446,9 @@ int prepare_cfg(const TablesView& tv, cudaStream_t st) {
   unsigned grid = (unsigned)((total + 255) / 256);
   if (grid > 148 * 32) grid = 148 * 32;
   k_prepare<C><<<grid, 256, 0, st>>>(tv.b, tv.g, tv.perminv, tv.E, tv.bmask, tv.scat);
-  return check_launch("k_prepare");
+  MCK_TRY(check_launch("k_prepare"));
+  if constexpr (ff_colored<C>()) return color_tables<C>(tv, st);
+  return MCK_OK;
 }
 
 int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st, bool validate) {
@@ -472,7 +557,7 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
   }
   FFParams p{};
   p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
-  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs;
+  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs; p.gcol = tv.gcol;
   p.scale = scale; p.norm = norm; p.out = out; p.ldo = ldo; p.E = tv.E; p.D = D;
   return launch_by_logn(p, logn, feat, fold, st);
 }
@@ -493,7 +578,7 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   if (e0 < 0 || ecount < 1 || e0 + ecount > tv.E) return fail_value("block range out of bounds");
   FFParams p{};
   p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
-  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs;
+  p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs; p.gcol = tv.gcol;
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
   return launch_by_logn(p, logn, false, fold, st);

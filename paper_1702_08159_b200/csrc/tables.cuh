@@ -22,7 +22,8 @@ struct TablesView {
   double* gnorm;     // [E]
   float* cs;         // [E][n]  C*scale (scale folded when it is a power of two)
   uint32_t* bmask;   // [E][words][T]  sign bits in layout-L register order
-  uint2* scat;       // [E][R][T]      {padded smem address of perm^-1[j], bits of g[perm^-1[j]]}
+  uint2* scat;       // [E][R][T]      {smem byte offset of element j's slot, bits of g[perm^-1[j]]}
+  uint32_t* gcol;    // [E][R/4][T]    gather slot colours (4 bytes per word; n >= 1024)
   int32_t* flag;     // validation flag
 };
 
@@ -50,6 +51,7 @@ inline int64_t tables_layout(int64_t n, int32_t E, char* base, TablesView* tv) {
   // sign masks: at most one 32-bit word per 32 elements, rounded up per thread
   v.bmask = (uint32_t*)take(((en + 31) / 32 + (int64_t)E * 64) * 4);
   v.scat = (uint2*)take(en * 8);
+  v.gcol = (uint32_t*)take(en);
   v.flag = (int32_t*)take(16);
   if (tv) *tv = v;
   return off;

@@ -132,3 +132,37 @@ class TestSharding:
         assert float(b.flat[-2]) == 3.0 and float(b.flat[-1]) == 4.0
         assert b.dw.data_ptr() == b.flat.data_ptr()
         assert isinstance(b.flat, torch.Tensor)
+
+
+@pytest.mark.parametrize("m,kind", [(32, "random"), (512, "random"), (32, "parallel"), (64, "strided")])
+def test_edge_colouring_of_permutation_graphs(lib, m, kind):
+    # the layout of Pi in shared memory (perm_color.cu): every scatter group
+    # and every gather group must see 32 distinct banks
+    n = 32 * m
+    rng = np.random.default_rng(m)
+    left = (np.arange(n) // 32).astype(np.int32)
+    if kind == "random":
+        right = (rng.permutation(n) // 32).astype(np.int32)
+    elif kind == "parallel":      # identity permutation: 32 parallel edges per pair
+        right = left.copy()
+    else:                         # transpose-like permutation
+        right = (np.arange(n) % m).astype(np.int32)
+    col = np.zeros(n, dtype=np.uint8)
+    def ptr(a):
+        return a.ctypes.data
+    rc = lib.mck_diag_edge_color32(m, ptr(left), ptr(right), ptr(col))
+    assert rc == 0
+    assert col.max() < 32
+    for side in (left, right):
+        pairs = side.astype(np.int64) * 32 + col
+        assert len(np.unique(pairs)) == n
+
+
+def test_edge_colouring_rejects_irregular_graph(lib):
+    def ptr(a):
+        return a.ctypes.data
+    m = 4
+    left = (np.arange(128) // 32).astype(np.int32)
+    right = np.zeros(128, dtype=np.int32)          # right node 0 has degree 128
+    col = np.zeros(128, dtype=np.uint8)
+    assert lib.mck_diag_edge_color32(m, ptr(left), ptr(right), ptr(col)) == 1
