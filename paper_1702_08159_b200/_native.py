@@ -8,10 +8,12 @@ CUDA device is present, calls raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libmckernel_b200.so"
+LIB_PATH = Path(os.environ.get("MCK_LIB_PATH") or
+                Path(__file__).resolve().parent / "libmckernel_b200.so")  # override: A/B experiments
 
 MCK_OK, MCK_ERR_VALUE, MCK_ERR_CUDA = 0, 1, 2
 MCK_KERNEL_RBF, MCK_KERNEL_MATERN = 0, 1

@@ -27,6 +27,7 @@ LIB = PKG / "libmckernel_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "-I", str(ROOT / "include")]
+FLAGS += os.environ.get("MCK_NVCC_EXTRA", "").split()  # A/B experiments only
 
 
 def nvcc() -> str:
@@ -54,6 +55,11 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
+    stamp = BUILD / "flags.txt"  # a change of flags rebuilds everything
+    flags = " ".join(ARCH + FLAGS)
+    if not stamp.exists() or stamp.read_text() != flags:
+        force = True
+        stamp.write_text(flags)
     sources = sorted(CSRC.glob("*.cu"))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:
         results = list(ex.map(lambda s: _compile(s, force), sources))

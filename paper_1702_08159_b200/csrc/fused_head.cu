@@ -8,7 +8,7 @@
 //                         contracted with the W slice of block e (shared
 //                         memory) into per-chunk partial logits
 //                       k_fused_fold: partial logits -> float64 logits
-//                         (fixed order: blocks ascending, chunks ascending)
+//                         (fixed order: blocks ascending, fixed tree over chunks)
 //   softmax / loss / delta (classifier.cu, k_head_softmax)
 //   for each block e:   k_fastfood again (recompute z; cheaper than storing
 //                         2^20 features per row)
@@ -144,13 +144,29 @@ __global__ void __launch_bounds__(kFwarps * 32) k_fused_fwd(const float* __restr
 }
 
 // logits[r][c] (+)= sum_ks lpart[ks][r][c]   (float64, chunk order)
-__global__ void k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C,
-                             double* logits, int first) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m * C) return;
-  double s = first ? 0.0 : logits[t];
-  for (int64_t k = 0; k < KS; ++k) s += (double)lpart[k * m * C + t];
-  logits[t] = s;
+// 32 outputs per CTA; warp w sums the partials k = w, w+8, ... and the eight
+// warp sums are combined in a fixed order (deterministic, independent loads).
+constexpr int kFoldWarps = 8;
+__global__ void __launch_bounds__(kFoldWarps * 32)
+k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C, double* logits,
+             int first) {
+  __shared__ double part[kFoldWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t mc = m * C;
+  const int64_t t = (int64_t)blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (t < mc) {
+#pragma unroll 4
+    for (int64_t k = w; k < KS; k += kFoldWarps) s += (double)lpart[k * mc + t];
+  }
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && t < mc) {
+    double r = first ? 0.0 : logits[t];
+#pragma unroll
+    for (int i = 0; i < kFoldWarps; ++i) r += part[i][lane];
+    logits[t] = r;
+  }
 }
 
 __global__ void k_to_f32(const double* a, float* b, int64_t n) {
@@ -292,8 +308,8 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                                                      D + (int64_t)e * n, fs.lpart);
       return check_launch("k_fused_fwd");
     }));
-    k_fused_fold<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(fs.lpart, KS, m, C, fs.logits,
-                                                                  e == 0 ? 1 : 0);
+    k_fused_fold<<<(unsigned)((m * C + 31) / 32), kFoldWarps * 32, 0, st>>>(
+        fs.lpart, KS, m, C, fs.logits, e == 0 ? 1 : 0);
     MCK_TRY(check_launch("k_fused_fold"));
   }
   if (logits_out)

@@ -1,19 +1,26 @@
 // K1 -- batched in-place Walsh-Hadamard transform (replaces wht.py:142-162).
 //
 // fast variant
-//   n <= 2^15 : one thread group per row (fwht_core.cuh), rows stay in
+//   n <= 2^14 : one thread group per row (fwht_core.cuh), rows stay in
 //               registers; 16-byte coalesced global loads/stores.
-//   n >= 2^16 : the row is viewed as [N1][N2] (N2 = 2^14).  Phase A
-//               transforms the N1-long columns (each thread one column, in
-//               registers); phase B runs the register kernel on the N1
-//               contiguous N2-segments.  Rows are processed in chunks small
-//               enough (<= 24 MiB) that phase B finds phase A's output in the
-//               126 MB L2, so HBM sees about one read and one write.
+//   2^15..2^18: one thread-block cluster of K = n/2^14 CTAs per row: each CTA
+//               transforms a 2^14-segment, then H_K across the segments via
+//               DSMEM (fwht_cluster_kernel); one HBM pass.
+//   2^19, 2^20: the row is viewed as [N1][2^14].  Phase A transforms the
+//               N1-long columns (registers; stores tagged L2 evict_last);
+//               phase B runs the register kernel on the N1 segments.  Chunks
+//               of <= 24 MiB keep phase A's output in the 126 MB L2 for
+//               phase B, which overlaps the next chunk's phase A on a side
+//               stream.
 // parity variant (verification only; bit-exact to the reference on
 //   OpenBLAS SkylakeX): every aligned base chunk (256) becomes the sequential
 //   fp32 sum over k of H[k][j]*x_k, then combine stages (a+b, (a+b)-2b).
 #include "mck_common.cuh"
 #include "fwht_core.cuh"
+
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
 
 namespace mck {
 
@@ -125,6 +132,25 @@ __device__ __forceinline__ void vadd(float4& a, float4& b) {
   vadd(a.x, b.x); vadd(a.y, b.y); vadd(a.z, b.z); vadd(a.w, b.w);
 }
 
+__device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float2* p, float2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
+               "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 template <int LOGN1, int VW, class V>
 __global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, int64_t rows,
                                                         int n2) {
@@ -145,8 +171,11 @@ __global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, in
       for (int i = 0; i < N1; ++i)
         if (!(i & h)) vadd(v[i], v[i | h]);
     }
+    // keep phase A's output resident in L2 for phase B
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
-    for (int i = 0; i < N1; ++i) p[(int64_t)i * vcols] = v[i];
+    for (int i = 0; i < N1; ++i) st_hint(&p[(int64_t)i * vcols], v[i], pol);
   }
 }
 
@@ -195,6 +224,118 @@ int launch_cols(V* data, int64_t rows, int logn1, int n2, cudaStream_t st) {
   }
 }
 
+// n = K * 2^14, K = 2..16 (fp32): one thread-block cluster of K CTAs per row,
+// a single HBM pass.  CTA c transforms its contiguous 2^14-segment with the
+// register/shared-memory kernel and parks the result in its shared memory;
+// after a cluster barrier it owns 1/K of the segment positions and applies
+// H_K across the K segments (segment index = the top log2 K index bits),
+// reading the peers' shared memory through DSMEM (16-byte loads) and writing
+// all K output segments of its share.  A second cluster barrier keeps every
+// CTA's shared memory alive until the peers have read it.
+template <int K>
+__global__ void __launch_bounds__(RowCfg<14, 5>::T)
+fwht_cluster_kernel(float* __restrict__ data, int64_t rows) {
+  using C = RowCfg<14, 5>;
+  constexpr int VW = K >= 16 ? 2 : 4;  // K vectors in registers
+  constexpr int SEG = C::N, SHAREV = SEG / K / VW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned c = cl.block_rank();
+  const int64_t row = blockIdx.x / K;
+  const uint32_t tid = threadIdx.x;
+  float* prow = data + row * (int64_t)(K * SEG);
+  float v[C::R];
+  load_row_L<C>(prow + (int64_t)c * SEG, tid, v);
+  butterflies<C::R, C::PL, C::PL>(v);
+  middle_rounds<C, 0, C::PL>(s, tid, 0, v);
+  // transform complete in layout PM, whose lanes run along index bits 0..4:
+  // scalar stores straight into the linear segment are conflict free
+  constexpr uint32_t PM = last_mid_regs<C>();
+  __syncthreads();
+  {
+    float* base = s + thread_part<C::FULL, PM>(tid);
+#pragma unroll
+    for (int k = 0; k < C::R; ++k) base[deposit_bits((uint32_t)k, PM)] = v[k];
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  using VT = typename VecT<float, VW>::T;
+  constexpr int ITER = (SHAREV + C::T - 1) / C::T;
+  VT a[ITER][K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const VT* seg = cl.map_shared_rank(reinterpret_cast<const VT*>(s), (unsigned)k) + c * SHAREV;
+#pragma unroll
+    for (int it = 0; it < ITER; ++it)
+      if (SHAREV % C::T == 0 || (int)tid + it * C::T < SHAREV) a[it][k] = seg[tid + it * C::T];
+  }
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+#pragma unroll
+    for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (!(k & h)) vadd(a[it][k], a[it][k | h]);
+  }
+  // every remote load has been consumed: peers may release their shared
+  // memory once all CTAs arrive (the global stores overlap the barrier)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int q = (int)tid + it * C::T;
+    if (SHAREV % C::T != 0 && q >= SHAREV) continue;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      reinterpret_cast<VT*>(prow + (int64_t)k * SEG)[c * SHAREV + q] = a[it][k];
+  }
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+template <int K>
+int launch_cluster_t(float* data, int64_t rows, cudaStream_t st) {
+  using C = RowCfg<14, 5>;
+  const size_t smem = (size_t)C::SMEM_FLOATS * sizeof(float);
+  auto kern = fwht_cluster_kernel<K>;
+  static bool init = false;
+  if (!init) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "fwht cluster smem"));
+    if (K > 8)
+      MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                         "fwht cluster size"));
+    init = true;
+  }
+  for (int64_t r0 = 0; r0 < rows; r0 += (1ll << 26)) {
+    const int64_t nr = rows - r0 < (1ll << 26) ? rows - r0 : (1ll << 26);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(nr * K));
+    cfg.blockDim = dim3(C::T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, data + r0 * (int64_t)K * C::N, nr),
+                       "fwht_cluster_kernel launch"));
+  }
+  return check_launch("fwht_cluster_kernel");
+}
+
+// Rows of 2^logn with 15 <= logn <= 18 in one pass (fp32).
+int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
+  switch (logn) {
+    case 15: return launch_cluster_t<2>(data, rows, st);
+    case 16: return launch_cluster_t<4>(data, rows, st);
+    case 17: return launch_cluster_t<8>(data, rows, st);
+    case 18: return launch_cluster_t<16>(data, rows, st);
+    default: return fail_value("internal: no cluster kernel for 2^%d", logn);
+  }
+}
+
 // Second stream used to overlap phase B of chunk k with phase A of chunk k+1.
 struct SideStreams {
   cudaStream_t s[16] = {};
@@ -222,6 +363,7 @@ __global__ void fwht_tiny_kernel(V* data, int64_t rows, int n) {
       if (!(i & h)) { V a = p[i], b = p[i | h]; p[i] = a + b; p[i | h] = a - b; }
 }
 
+
 template <class V>
 int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
   int logn = 0;
@@ -231,6 +373,9 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
   if (logn <= 2) {
     fwht_tiny_kernel<V><<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(data, rows, (int)n);
     return check_launch("fwht_tiny_kernel");
+  }
+  if constexpr (sizeof(V) == 4) {
+    if (logn >= 15 && logn <= 18) return launch_cluster(data, rows, logn, st);
   }
   if (logn <= max_row_logn) return launch_rows_by_logn<V>(data, rows, logn, st);
   const int logn2 = 14, logn1 = logn - logn2;

@@ -154,6 +154,16 @@ class TestWht:
             ss = float((y.astype(np.float64) ** 2).sum())
             assert abs(ss - float(z[f"n{k}.sumsq"][0])) <= 1e-5 * ss
 
+    def test_cluster_sizes_multi_row(self, cuda):
+        # 2^15..2^18 run as one thread-block cluster per row (DSMEM combine);
+        # 2^19 as column pass + cluster rows
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        for k in range(15, 20):
+            x = synthetic.gaussian_rows(5, 1 << k, seed=300 + k)
+            got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+            _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
+
     def test_parity_variant_bit_exact(self, cuda):
         from paper_1702_08159_b200 import wht_fast_batch
         torch = cuda
