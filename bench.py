@@ -332,8 +332,10 @@ def extras(args, P, torch, dev, hbm):
         tr.step(0, s)
     torch.cuda.synchronize()
     t_steps = time_cuda(lambda: [tr.step(1, s) for s in range(tr.steps)], 1, torch)
+    tr.evaluate()  # first call allocates the evaluation buffers
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tr.evaluate()
+    tr.evaluate()  # returns host scalars (synchronises)
     t_eval = (time.perf_counter() - t0) * 1e3
     out["c3_train"] = {"ms_per_epoch_steps": round(t_steps, 3), "ms_eval": round(t_eval, 3),
                        "ms_per_step": round(t_steps / tr.steps, 4),
