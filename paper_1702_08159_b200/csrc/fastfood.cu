@@ -39,6 +39,9 @@ constexpr int ff_rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
 // scatter to the padded layout and gather with the structured layout read.
 template <class C>
 constexpr bool ff_colored() { return C::T >= 32; }
+// n = 1024 runs the two-rows-per-thread kernel (k_fastfood_pair)
+template <class C>
+constexpr bool ff_pair() { return C::LOGN == 10 && C::LOGR == 5; }
 template <class C>
 constexpr int bm_stride() { return ((((C::R + 31) / 32) * C::T) + 3) & ~3; }
 template <class C>
@@ -324,6 +327,249 @@ k_fastfood(FFParams p) {
   }
 }
 
+// ---------------------------------------------------------------- two rows per thread
+// n = 1024.  Each warp owns TWO rows; register k holds the pair (row0[i],
+// row1[i]) of one index i, so every butterfly stage is a packed f32x2 add/sub
+// (including the stage on the lowest register bit that the one-row kernel
+// leaves scalar), every exchange moves both rows with one 8-byte access, and
+// each table entry (scatter offset + g, gather colour, C*scale, sign mask) is
+// loaded once for two rows.  x is re-read per block (L1-resident) instead of
+// being held in registers.  Exchanges use the 8-byte padding pad2 (conflict
+// free per 16-lane phase for layouts L and P0); Pi uses 16-colour slots.
+__host__ __device__ constexpr uint32_t pad2(uint32_t i) { return i + (i >> 4) + 4 * (i >> 7); }
+constexpr int kPairRowFloat2 = 1116;  // pad2(1023) + 1, rounded to 16 bytes
+constexpr int kPairWarps = 8;
+
+template <int R, uint32_t P, uint32_t ACTIVE>
+__device__ __forceinline__ void butterflies2(float2 (&v)[R]) {
+#pragma unroll
+  for (int a = 0; (1 << a) < R; ++a) {
+    if (ACTIVE & deposit_bits(1u << a, P)) {
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (!(k & (1 << a))) bfly_pk(v[k].x, v[k].y, v[k | (1 << a)].x, v[k | (1 << a)].y);
+    }
+  }
+}
+
+template <int R, uint32_t P>
+__device__ __forceinline__ void sts2(float2* s, uint32_t tpart, const float2 (&v)[R]) {
+  float2* base = s + pad2(tpart);
+#pragma unroll
+  for (int k = 0; k < R; ++k) base[pad2(deposit_bits((uint32_t)k, P))] = v[k];
+}
+
+template <int R, uint32_t P>
+__device__ __forceinline__ void lds2(const float2* s, uint32_t tpart, float2 (&v)[R]) {
+  const float2* base = s + pad2(tpart);
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = base[pad2(deposit_bits((uint32_t)k, P))];
+}
+
+template <class C>
+constexpr size_t ff_pair_smem_bytes() {
+  return 128 + 2 * (size_t)tab_slot<C>() + (size_t)kPairWarps * kPairRowFloat2 * 8;
+}
+
+template <bool FEAT, bool FOLD, bool VEC>
+__global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p) {
+  using C = RowCfg<10, 5>;
+  constexpr int R = C::R, T = C::T, N = C::N;
+  constexpr int ROWS = 2 * kPairWarps;
+  constexpr int SLOT = tab_slot<C>();
+  constexpr uint32_t PL = C::PL, P0 = C::mid_regs(0);
+  static_assert(C::NMID == 1 && T == 32, "pair kernel layout");
+  extern __shared__ __align__(128) unsigned char ff_smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ff_smem);
+  unsigned char* tabs = ff_smem + 128;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  float2* s = reinterpret_cast<float2*>(ff_smem + 128 + 2 * SLOT) + warp * kPairRowFloat2;
+  const uint32_t tp_l = thread_part<C::FULL, PL>(lane), tp_0 = thread_part<C::FULL, P0>(lane);
+
+  // Work items (row group of 16, block e), group-major; each CTA takes a
+  // contiguous, balanced range (x stays L1-resident while the group is the
+  // same; no per-group tail).
+  const int64_t groups = (p.m + ROWS - 1) / ROWS;
+  const int64_t items = groups * p.E;
+  const int64_t it_lo = items * blockIdx.x / gridDim.x, it_hi = items * (blockIdx.x + 1) / gridDim.x;
+  auto issue = [&](int64_t it) {  // thread 0 only; buffer = parity of the local index
+    const int e = p.e0 + (int)(it % p.E);
+    const int64_t li = it - it_lo;
+    unsigned char* dst = tabs + (li & 1) * SLOT;
+    uint64_t* b = bar + (li & 1);
+    mbar_expect_tx(b, tab_bytes<C>());
+    bulk_g2s(dst, p.scat + (int64_t)e * N, N * 8, b);
+    bulk_g2s(dst + N * 8, p.cs + (int64_t)e * N, N * 4, b);
+    bulk_g2s(dst + N * 12, p.bmask + (int64_t)e * bm_stride<C>(), bm_stride<C>() * 4, b);
+    bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)e * (N / 4), N, b);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && it_lo < it_hi) issue(it_lo);
+
+  for (int64_t it = it_lo; it < it_hi; ++it) {
+    const int64_t li = it - it_lo;
+    const int64_t gi = it / p.E;
+    const int e = (int)(it % p.E);
+    const int64_t row0 = gi * ROWS + 2 * warp;
+    const bool v0 = row0 < p.m, v1 = row0 + 1 < p.m;
+    const float* xp0 = p.x + (v0 ? (p.rows ? (int64_t)p.rows[row0] : row0) : 0) * p.ldx;
+    const float* xp1 = p.x + (v1 ? (p.rows ? (int64_t)p.rows[row0 + 1] : row0 + 1) : 0) * p.ldx;
+    float* const orow0 = p.out + (v0 ? row0 : 0) * p.ldo;
+    float* const orow1 = p.out + (v1 ? row0 + 1 : 0) * p.ldo;
+    {
+      // ---- x (layout L, both rows): loads issued before the table wait
+      float2 v[R];
+#pragma unroll
+      for (int j = 0; j < R / 4; ++j) {
+        const int i0 = 4 * (int)lane + j * 4 * T;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if constexpr (VEC) {
+          if (v0 && i0 < p.d) a = __ldg(reinterpret_cast<const float4*>(xp0 + i0));
+          if (v1 && i0 < p.d) b = __ldg(reinterpret_cast<const float4*>(xp1 + i0));
+        } else {
+          a.x = (v0 && i0 < p.d) ? __ldg(xp0 + i0) : 0.f;
+          a.y = (v0 && i0 + 1 < p.d) ? __ldg(xp0 + i0 + 1) : 0.f;
+          a.z = (v0 && i0 + 2 < p.d) ? __ldg(xp0 + i0 + 2) : 0.f;
+          a.w = (v0 && i0 + 3 < p.d) ? __ldg(xp0 + i0 + 3) : 0.f;
+          b.x = (v1 && i0 < p.d) ? __ldg(xp1 + i0) : 0.f;
+          b.y = (v1 && i0 + 1 < p.d) ? __ldg(xp1 + i0 + 1) : 0.f;
+          b.z = (v1 && i0 + 2 < p.d) ? __ldg(xp1 + i0 + 2) : 0.f;
+          b.w = (v1 && i0 + 3 < p.d) ? __ldg(xp1 + i0 + 3) : 0.f;
+        }
+        v[4 * j] = make_float2(a.x, b.x);
+        v[4 * j + 1] = make_float2(a.y, b.y);
+        v[4 * j + 2] = make_float2(a.z, b.z);
+        v[4 * j + 3] = make_float2(a.w, b.w);
+      }
+      __syncthreads();  // buffer (li+1)&1 (read at li-1) is free
+      if (threadIdx.x == 0 && it + 1 < it_hi) issue(it + 1);
+      mbar_wait(bar + (li & 1), (uint32_t)((li >> 1) & 1));
+      const unsigned char* tb = tabs + (li & 1) * SLOT;
+      const uint2* t_scat = reinterpret_cast<const uint2*>(tb);
+      const float* t_cs = reinterpret_cast<const float*>(tb + N * 8);
+      const uint32_t* t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
+      const uint32_t* t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
+
+      // ---- x * B (sign XOR, exact; one mask word for both rows)
+      const uint32_t bits = t_bm[lane];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const uint32_t sg = ((bits >> k) & 1u) << 31;
+        v[k].x = __uint_as_float(__float_as_uint(v[k].x) ^ sg);
+        v[k].y = __uint_as_float(__float_as_uint(v[k].y) ^ sg);
+      }
+      // ---- H (first): layout L rounds, exchange, round P0
+      butterflies2<R, PL, PL>(v);
+      sts2<R, PL>(s, tp_l, v);
+      __syncwarp();
+      lds2<R, P0>(s, tp_0, v);
+      __syncwarp();
+      butterflies2<R, P0, P0>(v);
+      // ---- Pi and G: scatter (coloured 8-byte slots), gather
+#pragma unroll
+      for (int k0 = 0; k0 < R; k0 += 8) {
+        uint2 a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + lane];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float2 w = v[k0 + q];
+          const float g = __uint_as_float(a[q].y);
+          mul_pk(w.x, w.y, g, g);
+          *reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + a[q].x) = w;
+        }
+      }
+      __syncwarp();
+      {
+        // gather group (register k, half-warp h) occupies 8-byte slots 16*(2k+h) + colour
+        const char* gb = reinterpret_cast<const char*>(s) + 128 * (lane >> 4);
+#pragma unroll
+        for (int k4 = 0; k4 < R / 4; ++k4) {
+          const uint32_t cw = t_gc[k4 * T + lane];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v[4 * k4 + q] = *reinterpret_cast<const float2*>(gb + (4 * k4 + q) * 256 + ((cw >> (8 * q)) & 0xffu));
+        }
+      }
+      __syncwarp();
+      // ---- H (second): round P0, exchange, layout L rounds
+      butterflies2<R, P0, P0>(v);
+      sts2<R, P0>(s, tp_0, v);
+      __syncwarp();
+      lds2<R, PL>(s, tp_l, v);
+      __syncwarp();
+      butterflies2<R, PL, PL>(v);
+      // ---- C * scale and the feature epilogue, both rows
+      float* const ob0 = orow0 + (int64_t)e * N + 4 * (int)lane;
+      float* const ob1 = orow1 + (int64_t)e * N + 4 * (int)lane;
+      const float* const csb = t_cs + 4 * (int)lane;
+#pragma unroll
+      for (int j = 0; j < R / 4; ++j) {
+        const float4 c4 = *reinterpret_cast<const float4*>(csb + j * 4 * T);
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+        float2 z[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          z[c] = v[4 * j + c];
+          mul_pk(z[c].x, z[c].y, cc[c], cc[c]);
+          if constexpr (!FOLD) mul_pk(z[c].x, z[c].y, p.scale, p.scale);
+        }
+        if constexpr (FEAT) {
+          float2 sn[4], cn[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sincos_fast(z[c].x, sn[c].x, cn[c].x);
+            sincos_fast(z[c].y, sn[c].y, cn[c].y);
+            mul_pk(sn[c].x, sn[c].y, p.norm, p.norm);
+            mul_pk(cn[c].x, cn[c].y, p.norm, p.norm);
+          }
+          if (v0) {
+            *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(cn[0].x, cn[1].x, cn[2].x, cn[3].x);
+            *reinterpret_cast<float4*>(ob0 + p.D + j * 4 * T) = make_float4(sn[0].x, sn[1].x, sn[2].x, sn[3].x);
+          }
+          if (v1) {
+            *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(cn[0].y, cn[1].y, cn[2].y, cn[3].y);
+            *reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T) = make_float4(sn[0].y, sn[1].y, sn[2].y, sn[3].y);
+          }
+        } else {
+          if (v0) *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
+          if (v1) *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(z[0].y, z[1].y, z[2].y, z[3].y);
+        }
+      }
+    }
+  }
+}
+
+template <bool FEAT, bool FOLD, bool VEC>
+int launch_ff_pair(const FFParams& p, cudaStream_t st) {
+  using C = RowCfg<10, 5>;
+  constexpr int ROWS = 2 * kPairWarps;
+  const size_t smem = ff_pair_smem_bytes<C>();
+  auto kern = k_fastfood_pair<FEAT, FOLD, VEC>;
+  static int occ = 0, sms = 0;
+  if (occ == 0) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "fastfood pair smem"));
+    int dev = 0;
+    MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
+    MCK_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms"));
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPairWarps * 32, smem),
+                       "occupancy"));
+    if (occ < 1) occ = 1;
+  }
+  const int64_t items = (p.m + ROWS - 1) / ROWS * p.E;
+  int64_t grid = (int64_t)sms * occ;
+  if (grid > items) grid = items;
+  kern<<<(unsigned)grid, kPairWarps * 32, smem, st>>>(p);
+  return check_launch("k_fastfood_pair");
+}
+
 // ---------------------------------------------------------------- parity variant
 // One CTA per (row, block); follows fastfood.py:189-197 operation by operation.
 __device__ void parity_wht_smem(float* a, float* tmp, int n) {
@@ -390,10 +636,13 @@ __global__ void k_fastfood_parity(const float* x, int64_t ldx, int32_t d, const 
 // leaves y[j] in (thread t, register k) of layout PM -> scatter group
 // S = (t/32)*R + k; position p = perm^-1[j] is read by (t', k') of layout P0
 // -> gather group G = (t'/32)*R + k'.  Slot = 32*G + colour(j).
-template <class C>
+template <class C, bool PAIR>
 int color_tables(const TablesView& tv, cudaStream_t st) {
-  constexpr int R = C::R, T = C::T, N = C::N, M = N / 32;
+  // PAIR: two rows per thread, 8-byte elements, conflicts per 16-lane phase
+  constexpr int R = C::R, T = C::T, N = C::N;
+  constexpr int GW = PAIR ? 16 : 32, ES = PAIR ? 8 : 4, LEVELS = PAIR ? 4 : 5, M = N / GW;
   constexpr uint32_t PM = last_mid_regs<C>(), P0 = C::mid_regs(0);
+  auto group = [](int t, int k) { return PAIR ? k * (T / GW) + t / GW : (t / 32) * R + k; };
   const int E = tv.E;
   std::vector<int32_t> pinv((size_t)E * N);
   std::vector<uint32_t> gbits((size_t)E * N);
@@ -406,10 +655,10 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
   for (int t = 0; t < T; ++t)
     for (int k = 0; k < R; ++k) {
       const uint32_t j = deposit_bits((uint32_t)t, C::FULL & ~PM) | deposit_bits((uint32_t)k, PM);
-      sgrp[j] = (t / 32) * R + k;
+      sgrp[j] = group(t, k);
       spos[j] = k * T + t;
       const uint32_t p = deposit_bits((uint32_t)t, C::FULL & ~P0) | deposit_bits((uint32_t)k, P0);
-      ggrp[p] = (t / 32) * R + k;
+      ggrp[p] = group(t, k);
       gpos[p] = k * T + t;
     }
   std::vector<uint2> scat((size_t)E * N);
@@ -422,14 +671,14 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
       left[j] = sgrp[j];
       right[j] = ggrp[pi[j]];
     }
-    if (!edge_color32(M, N, left.data(), right.data(), col.data()))
+    if (!edge_color_pow2(M, LEVELS, N, left.data(), right.data(), col.data()))
       return fail_value("internal: permutation edge colouring failed (block %d)", e);
     for (int j = 0; j < N; ++j) {
       const int32_t p = pi[j];
       scat[(size_t)e * N + spos[j]] =
-          make_uint2(4u * (32u * (uint32_t)ggrp[p] + col[j]), gbits[(size_t)e * N + p]);
+          make_uint2((uint32_t)ES * ((uint32_t)GW * (uint32_t)ggrp[p] + col[j]), gbits[(size_t)e * N + p]);
       const int k = gpos[p] / T, t = gpos[p] % T;
-      gcol[(size_t)e * (N / 4) + (k / 4) * T + t] |= (4u * col[j]) << (8 * (k % 4));
+      gcol[(size_t)e * (N / 4) + (k / 4) * T + t] |= ((uint32_t)ES * col[j]) << (8 * (k % 4));
     }
   }
   MCK_TRY(check_cuda(cudaMemcpyAsync(tv.scat, scat.data(), scat.size() * 8,
@@ -447,7 +696,7 @@ int prepare_cfg(const TablesView& tv, cudaStream_t st) {
   if (grid > 148 * 32) grid = 148 * 32;
   k_prepare<C><<<grid, 256, 0, st>>>(tv.b, tv.g, tv.perminv, tv.E, tv.bmask, tv.scat);
   MCK_TRY(check_launch("k_prepare"));
-  if constexpr (ff_colored<C>()) return color_tables<C>(tv, st);
+  if constexpr (ff_colored<C>()) return color_tables<C, ff_pair<C>()>(tv, st);
   return MCK_OK;
 }
 
@@ -512,12 +761,21 @@ int launch_ff(const FFParams& p, cudaStream_t st) {
 
 template <class C>
 int launch_ff_cfg(const FFParams& p, bool feat, bool fold, bool vec, cudaStream_t st) {
+  if constexpr (ff_pair<C>()) {
+    if (feat) {
+      if (fold) return vec ? launch_ff_pair<true, true, true>(p, st) : launch_ff_pair<true, true, false>(p, st);
+      return vec ? launch_ff_pair<true, false, true>(p, st) : launch_ff_pair<true, false, false>(p, st);
+    }
+    if (fold) return vec ? launch_ff_pair<false, true, true>(p, st) : launch_ff_pair<false, true, false>(p, st);
+    return vec ? launch_ff_pair<false, false, true>(p, st) : launch_ff_pair<false, false, false>(p, st);
+  } else {
   if (feat) {
     if (fold) return vec ? launch_ff<C, true, true, true>(p, st) : launch_ff<C, true, true, false>(p, st);
     return vec ? launch_ff<C, true, false, true>(p, st) : launch_ff<C, true, false, false>(p, st);
   }
   if (fold) return vec ? launch_ff<C, false, true, true>(p, st) : launch_ff<C, false, true, false>(p, st);
   return vec ? launch_ff<C, false, false, true>(p, st) : launch_ff<C, false, false, false>(p, st);
+  }
 }
 
 int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream_t st);

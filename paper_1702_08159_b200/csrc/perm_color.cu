@@ -11,8 +11,10 @@
 //
 // Colouring by repeated Euler splits: in a 2^k-regular bipartite multigraph,
 // walking closed trails and sending left->right edges to one half and
-// right->left edges to the other leaves two 2^(k-1)-regular halves; five
-// levels give 32 perfect matchings = colours.  O(n log 32) per block.
+// right->left edges to the other leaves two 2^(k-1)-regular halves; k
+// levels give 2^k perfect matchings = colours.  O(n k) per block.  Degree 32
+// serves one-row warps (4-byte slots), degree 16 the two-row kernel's
+// half-warp phases (8-byte slots).
 #include <algorithm>
 #include <cstdint>
 #include <vector>
@@ -21,13 +23,15 @@
 
 namespace mck {
 
-bool edge_color32(int m, int64_t nedges, const int32_t* l, const int32_t* r, uint8_t* col) {
-  if (nedges != (int64_t)m * 32) return false;
+bool edge_color_pow2(int m, int levels, int64_t nedges, const int32_t* l, const int32_t* r,
+                     uint8_t* col) {
+  const int deg = 1 << levels;
+  if (levels < 0 || levels > 7 || nedges != (int64_t)m * deg) return false;
   const int64_t n = nedges;
   std::vector<int32_t> cls(n, 0);
   std::vector<int32_t> start, fill, adj(2 * n);
   std::vector<uint8_t> used(n), side(n);
-  for (int lev = 0; lev < 5; ++lev) {
+  for (int lev = 0; lev < levels; ++lev) {
     const int64_t keys = ((int64_t)1 << lev) * 2 * m;
     auto key_l = [&](int64_t e) { return (int64_t)cls[e] * 2 * m + l[e]; };
     auto key_r = [&](int64_t e) { return (int64_t)cls[e] * 2 * m + m + r[e]; };
@@ -60,11 +64,11 @@ bool edge_color32(int m, int64_t nedges, const int32_t* l, const int32_t* r, uin
     for (int64_t e = 0; e < n; ++e) cls[e] = 2 * cls[e] + side[e];
   }
   // verify: every (node, colour) pair used exactly once on both sides
-  std::vector<uint8_t> seen((size_t)m * 32 * 2, 0);
+  std::vector<uint8_t> seen((size_t)m * deg * 2, 0);
   for (int64_t e = 0; e < n; ++e) {
     if (l[e] < 0 || l[e] >= m || r[e] < 0 || r[e] >= m) return false;
-    uint8_t& a = seen[((size_t)l[e] * 32 + cls[e]) * 2];
-    uint8_t& b = seen[((size_t)r[e] * 32 + cls[e]) * 2 + 1];
+    uint8_t& a = seen[((size_t)l[e] * deg + cls[e]) * 2];
+    uint8_t& b = seen[((size_t)r[e] * deg + cls[e]) * 2 + 1];
     if (a || b) return false;
     a = b = 1;
     col[e] = (uint8_t)cls[e];
@@ -75,5 +79,5 @@ bool edge_color32(int m, int64_t nedges, const int32_t* l, const int32_t* r, uin
 }  // namespace mck
 
 extern "C" int mck_diag_edge_color32(int32_t m, const int32_t* l, const int32_t* r, uint8_t* col) {
-  return mck::edge_color32(m, (int64_t)m * 32, l, r, col) ? 0 : 1;
+  return mck::edge_color_pow2(m, 5, (int64_t)m * 32, l, r, col) ? 0 : 1;
 }

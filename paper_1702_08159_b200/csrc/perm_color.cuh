@@ -5,9 +5,10 @@
 
 namespace mck {
 
-// Proper 32-edge-colouring of a 32-regular bipartite multigraph with m nodes
-// per side; edge e joins left l[e] to right r[e].  Returns false if the graph
-// is not 32-regular (the result is verified before returning true).
-bool edge_color32(int m, int64_t nedges, const int32_t* l, const int32_t* r, uint8_t* col);
+// Proper 2^levels-edge-colouring of a 2^levels-regular bipartite multigraph
+// with m nodes per side; edge e joins left l[e] to right r[e].  Returns false
+// if the graph is not regular (the result is verified before returning true).
+bool edge_color_pow2(int m, int levels, int64_t nedges, const int32_t* l, const int32_t* r,
+                     uint8_t* col);
 
 }  // namespace mck
