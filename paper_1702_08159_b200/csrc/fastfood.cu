@@ -423,7 +423,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
     float* const orow0 = p.out + (v0 ? row0 : 0) * p.ldo;
     float* const orow1 = p.out + (v1 ? row0 + 1 : 0) * p.ldo;
     {
-      // ---- x (layout L, both rows): loads issued before the table wait
+      // ---- x (layout L, both rows) * B, before the table wait: the sign word
+      // comes straight from global memory (L1) so the XOR writes the pair
+      // registers directly
+      const uint32_t bits = __ldg(p.bmask + (int64_t)(p.e0 + e) * bm_stride<C>() + lane);
       float2 v[R];
 #pragma unroll
       for (int j = 0; j < R / 4; ++j) {
@@ -442,10 +445,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
           b.z = (v1 && i0 + 2 < p.d) ? __ldg(xp1 + i0 + 2) : 0.f;
           b.w = (v1 && i0 + 3 < p.d) ? __ldg(xp1 + i0 + 3) : 0.f;
         }
-        v[4 * j] = make_float2(a.x, b.x);
-        v[4 * j + 1] = make_float2(a.y, b.y);
-        v[4 * j + 2] = make_float2(a.z, b.z);
-        v[4 * j + 3] = make_float2(a.w, b.w);
+        const float xa[4] = {a.x, a.y, a.z, a.w}, xb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t sg = ((bits >> (4 * j + c)) & 1u) << 31;
+          v[4 * j + c] = make_float2(__uint_as_float(__float_as_uint(xa[c]) ^ sg),
+                                     __uint_as_float(__float_as_uint(xb[c]) ^ sg));
+        }
       }
       __syncthreads();  // buffer (li+1)&1 (read at li-1) is free
       if (threadIdx.x == 0 && it + 1 < it_hi) issue(it + 1);
@@ -456,14 +462,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
       const uint32_t* t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
       const uint32_t* t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
 
-      // ---- x * B (sign XOR, exact; one mask word for both rows)
-      const uint32_t bits = t_bm[lane];
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        const uint32_t sg = ((bits >> k) & 1u) << 31;
-        v[k].x = __uint_as_float(__float_as_uint(v[k].x) ^ sg);
-        v[k].y = __uint_as_float(__float_as_uint(v[k].y) ^ sg);
-      }
       // ---- H (first): layout L rounds, exchange, round P0
       butterflies2<R, PL, PL>(v);
       sts2<R, PL>(s, tp_l, v);
@@ -521,21 +519,28 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
           if constexpr (!FOLD) mul_pk(z[c].x, z[c].y, p.scale, p.scale);
         }
         if constexpr (FEAT) {
-          float2 sn[4], cn[4];
+          // sin/cos per value, then the 1/sqrt(D) multiplies paired in store
+          // order so the products land in the 16-byte store registers
+          float c0[4], s0[4], c1[4], s1[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            sincos_fast(z[c].x, sn[c].x, cn[c].x);
-            sincos_fast(z[c].y, sn[c].y, cn[c].y);
-            mul_pk(sn[c].x, sn[c].y, p.norm, p.norm);
-            mul_pk(cn[c].x, cn[c].y, p.norm, p.norm);
+            sincos_fast(z[c].x, s0[c], c0[c]);
+            sincos_fast(z[c].y, s1[c], c1[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; c += 2) {
+            mul_pk(c0[c], c0[c + 1], p.norm, p.norm);
+            mul_pk(s0[c], s0[c + 1], p.norm, p.norm);
+            mul_pk(c1[c], c1[c + 1], p.norm, p.norm);
+            mul_pk(s1[c], s1[c + 1], p.norm, p.norm);
           }
           if (v0) {
-            *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(cn[0].x, cn[1].x, cn[2].x, cn[3].x);
-            *reinterpret_cast<float4*>(ob0 + p.D + j * 4 * T) = make_float4(sn[0].x, sn[1].x, sn[2].x, sn[3].x);
+            *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(c0[0], c0[1], c0[2], c0[3]);
+            *reinterpret_cast<float4*>(ob0 + p.D + j * 4 * T) = make_float4(s0[0], s0[1], s0[2], s0[3]);
           }
           if (v1) {
-            *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(cn[0].y, cn[1].y, cn[2].y, cn[3].y);
-            *reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T) = make_float4(sn[0].y, sn[1].y, sn[2].y, sn[3].y);
+            *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(c1[0], c1[1], c1[2], c1[3]);
+            *reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T) = make_float4(s1[0], s1[1], s1[2], s1[3]);
           }
         } else {
           if (v0) *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
