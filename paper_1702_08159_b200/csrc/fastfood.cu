@@ -147,6 +147,7 @@ struct FFParams {
   int32_t E;   // blocks computed: e0 .. e0+E-1, written at columns (e-e0)*n
   int64_t D;
   int32_t e0;
+  int32_t keep_l2;  // z stores tagged L2 evict_last (fused path: the tile is re-read next)
 };
 
 // Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
@@ -169,6 +170,7 @@ k_fastfood(FFParams p) {
   unsigned char* tabs = ff_smem + 128;
   const int gid = threadIdx.x / T;
   const uint32_t tid = threadIdx.x % T;
+  const uint64_t pol = FEAT ? 0ull : l2_policy_evict_last();
   float* s = reinterpret_cast<float*>(ff_smem + (STAGED ? 128 + 2 * SLOT : 0)) + gid * C::SMEM_FLOATS;
   constexpr uint32_t P0 = C::mid_regs(0);
 
@@ -319,8 +321,10 @@ k_fastfood(FFParams p) {
             *reinterpret_cast<float4*>(ob + j * 4 * T) = make_float4(cn[0], cn[1], cn[2], cn[3]);
             *reinterpret_cast<float4*>(obs + j * 4 * T) = make_float4(sn[0], sn[1], sn[2], sn[3]);
           }
-        } else {
-          if (valid) *reinterpret_cast<float4*>(ob + j * 4 * T) = make_float4(z[0], z[1], z[2], z[3]);
+        } else if (valid) {
+          const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
+          if (p.keep_l2) st_hint(reinterpret_cast<float4*>(ob + j * 4 * T), z4, pol);
+          else *reinterpret_cast<float4*>(ob + j * 4 * T) = z4;
         }
       }
     }
@@ -386,6 +390,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   const uint32_t lane = threadIdx.x & 31;
   float2* s = reinterpret_cast<float2*>(ff_smem + 128 + 2 * SLOT) + warp * kPairRowFloat2;
   const uint32_t tp_l = thread_part<C::FULL, PL>(lane), tp_0 = thread_part<C::FULL, P0>(lane);
+  const uint64_t pol = FEAT ? 0ull : l2_policy_evict_last();
 
   // Work items (row group of 16, block e), group-major; each CTA takes a
   // contiguous, balanced range (x stays L1-resident while the group is the
@@ -543,8 +548,15 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
             *reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T) = make_float4(s1[0], s1[1], s1[2], s1[3]);
           }
         } else {
-          if (v0) *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
-          if (v1) *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(z[0].y, z[1].y, z[2].y, z[3].y);
+          const float4 a = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
+          const float4 b = make_float4(z[0].y, z[1].y, z[2].y, z[3].y);
+          if (p.keep_l2) {
+            if (v0) st_hint(reinterpret_cast<float4*>(ob0 + j * 4 * T), a, pol);
+            if (v1) st_hint(reinterpret_cast<float4*>(ob1 + j * 4 * T), b, pol);
+          } else {
+            if (v0) *reinterpret_cast<float4*>(ob0 + j * 4 * T) = a;
+            if (v1) *reinterpret_cast<float4*>(ob1 + j * 4 * T) = b;
+          }
         }
       }
     }
@@ -844,6 +856,7 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs; p.gcol = tv.gcol;
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
+  p.keep_l2 = 1;
   return launch_by_logn(p, logn, false, fold, st);
 }
 

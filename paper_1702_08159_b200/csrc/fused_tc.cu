@@ -65,12 +65,12 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   auto load_stage = [&](int st, float4 (&dst)[2]) {
     const int zi = st * kFzStage + half * 8;
     if (zi + 8 <= nz) {
-      dst[0] = __ldg(reinterpret_cast<const float4*>(zr + zi));
-      dst[1] = __ldg(reinterpret_cast<const float4*>(zr + zi + 4));
+      dst[0] = __ldcs(reinterpret_cast<const float4*>(zr + zi));
+      dst[1] = __ldcs(reinterpret_cast<const float4*>(zr + zi + 4));
     } else {
       float tmp[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) tmp[j] = zi + j < nz ? __ldg(zr + zi + j) : 0.f;
+      for (int j = 0; j < 8; ++j) tmp[j] = zi + j < nz ? __ldcs(zr + zi + j) : 0.f;
       dst[0] = make_float4(tmp[0], tmp[1], tmp[2], tmp[3]);
       dst[1] = make_float4(tmp[4], tmp[5], tmp[6], tmp[7]);
     }
@@ -214,7 +214,7 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int64_t r = (int64_t)st * kBrowStage + 4 * (q0 + 4 * h) + j;
-        dst[4 * h + j] = (zok && r < m) ? __ldg(z + r * n + z0 + zi) : 0.f;
+        dst[4 * h + j] = (zok && r < m) ? __ldcs(z + r * n + z0 + zi) : 0.f;
       }
   };
 #pragma unroll

@@ -132,25 +132,6 @@ __device__ __forceinline__ void vadd(float4& a, float4& b) {
   vadd(a.x, b.x); vadd(a.y, b.y); vadd(a.z, b.z); vadd(a.w, b.w);
 }
 
-__device__ __forceinline__ void st_hint(float4* p, float4 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(float2* p, float2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
-               "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
-               "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-
 template <int LOGN1, int VW, class V>
 __global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, int64_t rows,
                                                         int n2) {
@@ -172,8 +153,7 @@ __global__ void __launch_bounds__(256) fwht_cols_kernel(V* __restrict__ data, in
         if (!(i & h)) vadd(v[i], v[i | h]);
     }
     // keep phase A's output resident in L2 for phase B
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    const uint64_t pol = l2_policy_evict_last();
 #pragma unroll
     for (int i = 0; i < N1; ++i) st_hint(&p[(int64_t)i * vcols], v[i], pol);
   }

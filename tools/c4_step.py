@@ -1,0 +1,23 @@
+"""Time the config-4 fused training step (1024 rows of one rank) and the c3 step."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+import paper_1702_08159_b200 as P
+from paper_1702_08159_b200.large_scale import FusedClassifier
+
+spec = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4)
+tc = "--cuda-cores" not in sys.argv
+fc = FusedClassifier(spec, 10, 1024, tensor_cores=tc)
+x = torch.randn((1024, 16384), device="cuda")
+y = torch.randint(0, 10, (1024,), device="cuda", dtype=torch.int32)
+for _ in range(2):
+    fc.step(x, y, m_total=8192, lr=0.01)
+torch.cuda.synchronize()
+s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+s.record()
+for _ in range(5):
+    fc.step(x, y, m_total=8192, lr=0.01)
+e.record()
+torch.cuda.synchronize()
+print(f"c4 step {s.elapsed_time(e) / 5:.3f} ms  (tensor_cores={tc})")
