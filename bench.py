@@ -201,7 +201,7 @@ def bench_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                "kernel": "k_fastfood<RowCfg<10,5>,FEAT=1,FOLD=1,VEC=1> (scale 1/64 folded into C)",
+                "kernel": "k_fastfood_pair<FEAT=1,FOLD=1,VEC=1> (n=1024, two rows per thread; scale 1/64 folded into C)",
                 "alg_bytes_per_launch": int(batch * bytes_per_row),
                 "avg_launch_us": round(tot_ms / (args.steps * len(spans)) * 1e3, 2)}
 
