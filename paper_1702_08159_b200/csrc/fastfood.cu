@@ -331,6 +331,16 @@ k_fastfood(FFParams p) {
   }
 }
 
+// Feature stores.  MCK_FF_STORE_CS=1 marks them streaming (evict-first), which
+// keeps the re-read inputs and tables resident in L2 (A/B switch).
+#ifndef MCK_FF_STORE_CS
+#define MCK_FF_STORE_CS 0
+#endif
+__device__ __forceinline__ void st_out(float4* p, float4 v) {
+  if constexpr (MCK_FF_STORE_CS) __stcs(p, v);
+  else *p = v;
+}
+
 // ---------------------------------------------------------------- two rows per thread
 // n = 1024.  Each warp owns TWO rows; register k holds the pair (row0[i],
 // row1[i]) of one index i, so every butterfly stage is a packed f32x2 add/sub
@@ -383,64 +393,104 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   constexpr int SLOT = tab_slot<C>();
   constexpr uint32_t PL = C::PL, P0 = C::mid_regs(0);
   static_assert(C::NMID == 1 && T == 32, "pair kernel layout");
+  static_assert(2 * N * 4 <= kPairRowFloat2 * 8, "x staging fits the exchange buffer");
   extern __shared__ __align__(128) unsigned char ff_smem[];
+  // header: table barriers [0,1], per-warp x barriers [2 .. 2+kPairWarps)
   uint64_t* bar = reinterpret_cast<uint64_t*>(ff_smem);
   unsigned char* tabs = ff_smem + 128;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  uint64_t* xbar = bar + 2 + warp;
   float2* s = reinterpret_cast<float2*>(ff_smem + 128 + 2 * SLOT) + warp * kPairRowFloat2;
+  float* const xs = reinterpret_cast<float*>(s);  // x staging: row0 [0,N), row1 [N,2N)
   const uint32_t tp_l = thread_part<C::FULL, PL>(lane), tp_0 = thread_part<C::FULL, P0>(lane);
   const uint64_t pol = FEAT ? 0ull : l2_policy_evict_last();
 
-  // Work items (row group of 16, block e), group-major; each CTA takes a
-  // contiguous, balanced range (x stays L1-resident while the group is the
-  // same; no per-group tail).
+  // Work units (block e, row group of 16), block-major: u = e * groups + g.
+  // Each CTA takes a contiguous, balanced range, so its factor tables change
+  // at most a few times (x of a batch is L2-resident and re-read per block).
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
-  const int64_t items = groups * p.E;
-  const int64_t it_lo = items * blockIdx.x / gridDim.x, it_hi = items * (blockIdx.x + 1) / gridDim.x;
-  auto issue = [&](int64_t it) {  // thread 0 only; buffer = parity of the local index
-    const int e = p.e0 + (int)(it % p.E);
-    const int64_t li = it - it_lo;
-    unsigned char* dst = tabs + (li & 1) * SLOT;
-    uint64_t* b = bar + (li & 1);
+  const int64_t units = groups * p.E;
+  const int64_t u_lo = units * blockIdx.x / gridDim.x, u_hi = units * (blockIdx.x + 1) / gridDim.x;
+  if (u_lo >= u_hi) return;
+  const int e_first = (int)(u_lo / groups), e_last = (int)((u_hi - 1) / groups);
+  auto issue_tab = [&](int e, int slot) {  // thread 0 only
+    const int eg = p.e0 + e;
+    unsigned char* dst = tabs + slot * SLOT;
+    uint64_t* b = bar + slot;
     mbar_expect_tx(b, tab_bytes<C>());
-    bulk_g2s(dst, p.scat + (int64_t)e * N, N * 8, b);
-    bulk_g2s(dst + N * 8, p.cs + (int64_t)e * N, N * 4, b);
-    bulk_g2s(dst + N * 12, p.bmask + (int64_t)e * bm_stride<C>(), bm_stride<C>() * 4, b);
-    bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)e * (N / 4), N, b);
+    bulk_g2s(dst, p.scat + (int64_t)eg * N, N * 8, b);
+    bulk_g2s(dst + N * 8, p.cs + (int64_t)eg * N, N * 4, b);
+    bulk_g2s(dst + N * 12, p.bmask + (int64_t)eg * bm_stride<C>(), bm_stride<C>() * 4, b);
+    bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)eg * (N / 4), N, b);
+  };
+  auto src_row = [&](int64_t r) -> const float* {
+    return p.x + (p.rows ? (int64_t)p.rows[r] : r) * p.ldx;
+  };
+  // x rows of unit u -> this warp's staging area (lane 0 only; VEC: 16-byte rows)
+  auto issue_x = [&](int64_t u) {
+    const int64_t r0 = (u % groups) * ROWS + 2 * warp;
+    const uint32_t rb = (uint32_t)p.d * 4u;
+    const uint32_t bytes = (r0 < p.m ? rb : 0u) + (r0 + 1 < p.m ? rb : 0u);
+    mbar_expect_tx(xbar, bytes);
+    if (r0 < p.m) bulk_g2s(xs, src_row(r0), rb, xbar);
+    if (r0 + 1 < p.m) bulk_g2s(xs + N, src_row(r0 + 1), rb, xbar);
   };
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int i = 0; i < 2 + kPairWarps; ++i) mbar_init(bar + i, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x == 0 && it_lo < it_hi) issue(it_lo);
+  if (threadIdx.x == 0) {
+    issue_tab(e_first, 0);
+    if (e_last > e_first) issue_tab(e_first + 1, 1);
+  }
+  if constexpr (VEC) {
+    if (lane == 0) issue_x(u_lo);
+  }
 
-  for (int64_t it = it_lo; it < it_hi; ++it) {
-    const int64_t li = it - it_lo;
-    const int64_t gi = it / p.E;
-    const int e = (int)(it % p.E);
-    const int64_t row0 = gi * ROWS + 2 * warp;
+  int ti = -1, e_cur = -1;
+  uint32_t xph = 0, bits = 0;
+  const uint2* t_scat = nullptr;
+  const float* t_cs = nullptr;
+  const uint32_t* t_gc = nullptr;
+  for (int64_t u = u_lo; u < u_hi; ++u) {
+    const int e = (int)(u / groups);
+    const int64_t row0 = (u % groups) * ROWS + 2 * warp;
     const bool v0 = row0 < p.m, v1 = row0 + 1 < p.m;
-    const float* xp0 = p.x + (v0 ? (p.rows ? (int64_t)p.rows[row0] : row0) : 0) * p.ldx;
-    const float* xp1 = p.x + (v1 ? (p.rows ? (int64_t)p.rows[row0 + 1] : row0 + 1) : 0) * p.ldx;
+    if (e != e_cur) {  // uniform across the CTA
+      if (ti >= 0) {
+        __syncthreads();  // every warp is done with slot ti&1 ... and slot (ti+1)&1 is free
+        if (threadIdx.x == 0 && e + 1 <= e_last) issue_tab(e + 1, ti & 1);
+      }
+      ++ti;
+      e_cur = e;
+      mbar_wait(bar + (ti & 1), (uint32_t)((ti >> 1) & 1));
+      const unsigned char* tb = tabs + (ti & 1) * SLOT;
+      t_scat = reinterpret_cast<const uint2*>(tb);
+      t_cs = reinterpret_cast<const float*>(tb + N * 8);
+      bits = reinterpret_cast<const uint32_t*>(tb + N * 12)[lane];
+      t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
+    }
     float* const orow0 = p.out + (v0 ? row0 : 0) * p.ldo;
     float* const orow1 = p.out + (v1 ? row0 + 1 : 0) * p.ldo;
     {
-      // ---- x (layout L, both rows) * B, before the table wait: the sign word
-      // comes straight from global memory (L1) so the XOR writes the pair
-      // registers directly
-      const uint32_t bits = __ldg(p.bmask + (int64_t)(p.e0 + e) * bm_stride<C>() + lane);
+      // ---- x (layout L, both rows) * B as a sign XOR
       float2 v[R];
+      if constexpr (VEC) {
+        mbar_wait(xbar, xph);
+        xph ^= 1u;
+      }
 #pragma unroll
       for (int j = 0; j < R / 4; ++j) {
         const int i0 = 4 * (int)lane + j * 4 * T;
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
         if constexpr (VEC) {
-          if (v0 && i0 < p.d) a = __ldg(reinterpret_cast<const float4*>(xp0 + i0));
-          if (v1 && i0 < p.d) b = __ldg(reinterpret_cast<const float4*>(xp1 + i0));
+          if (v0 && i0 < p.d) a = *reinterpret_cast<const float4*>(xs + i0);
+          if (v1 && i0 < p.d) b = *reinterpret_cast<const float4*>(xs + N + i0);
         } else {
+          const float* xp0 = src_row(v0 ? row0 : 0);
+          const float* xp1 = src_row(v1 ? row0 + 1 : 0);
           a.x = (v0 && i0 < p.d) ? __ldg(xp0 + i0) : 0.f;
           a.y = (v0 && i0 + 1 < p.d) ? __ldg(xp0 + i0 + 1) : 0.f;
           a.z = (v0 && i0 + 2 < p.d) ? __ldg(xp0 + i0 + 2) : 0.f;
@@ -458,14 +508,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
                                      __uint_as_float(__float_as_uint(xb[c]) ^ sg));
         }
       }
-      __syncthreads();  // buffer (li+1)&1 (read at li-1) is free
-      if (threadIdx.x == 0 && it + 1 < it_hi) issue(it + 1);
-      mbar_wait(bar + (li & 1), (uint32_t)((li >> 1) & 1));
-      const unsigned char* tb = tabs + (li & 1) * SLOT;
-      const uint2* t_scat = reinterpret_cast<const uint2*>(tb);
-      const float* t_cs = reinterpret_cast<const float*>(tb + N * 8);
-      const uint32_t* t_bm = reinterpret_cast<const uint32_t*>(tb + N * 12);
-      const uint32_t* t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
+      if constexpr (VEC) __syncwarp();  // staging reads done before the exchange writes
 
       // ---- H (first): layout L rounds, exchange, round P0
       butterflies2<R, PL, PL>(v);
@@ -506,7 +549,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
       sts2<R, P0>(s, tp_0, v);
       __syncwarp();
       lds2<R, PL>(s, tp_l, v);
+      if constexpr (VEC) fence_proxy_async_smem();  // exchange reads before the next x copy
       __syncwarp();
+      if constexpr (VEC) {
+        // next unit's x streams into the (now free) exchange buffer during the epilogue
+        if (lane == 0 && u + 1 < u_hi) issue_x(u + 1);
+      }
       butterflies2<R, PL, PL>(v);
       // ---- C * scale and the feature epilogue, both rows
       float* const ob0 = orow0 + (int64_t)e * N + 4 * (int)lane;
@@ -540,12 +588,12 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
             mul_pk(s1[c], s1[c + 1], p.norm, p.norm);
           }
           if (v0) {
-            *reinterpret_cast<float4*>(ob0 + j * 4 * T) = make_float4(c0[0], c0[1], c0[2], c0[3]);
-            *reinterpret_cast<float4*>(ob0 + p.D + j * 4 * T) = make_float4(s0[0], s0[1], s0[2], s0[3]);
+            st_out(reinterpret_cast<float4*>(ob0 + j * 4 * T), make_float4(c0[0], c0[1], c0[2], c0[3]));
+            st_out(reinterpret_cast<float4*>(ob0 + p.D + j * 4 * T), make_float4(s0[0], s0[1], s0[2], s0[3]));
           }
           if (v1) {
-            *reinterpret_cast<float4*>(ob1 + j * 4 * T) = make_float4(c1[0], c1[1], c1[2], c1[3]);
-            *reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T) = make_float4(s1[0], s1[1], s1[2], s1[3]);
+            st_out(reinterpret_cast<float4*>(ob1 + j * 4 * T), make_float4(c1[0], c1[1], c1[2], c1[3]));
+            st_out(reinterpret_cast<float4*>(ob1 + p.D + j * 4 * T), make_float4(s1[0], s1[1], s1[2], s1[3]));
           }
         } else {
           const float4 a = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
