@@ -331,6 +331,13 @@ k_fastfood(FFParams p) {
   }
 }
 
+// x ^ (t & 0x80000000) in one LOP3.
+__device__ __forceinline__ uint32_t xor_sign(uint32_t x, uint32_t t) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(x), "r"(t), "n"(0x80000000u));
+  return r;
+}
+
 // Feature stores.  MCK_FF_STORE_CS=1 marks them streaming (evict-first), which
 // keeps the re-read inputs and tables resident in L2 (A/B switch).
 #ifndef MCK_FF_STORE_CS
@@ -428,8 +435,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
     return p.x + (p.rows ? (int64_t)p.rows[r] : r) * p.ldx;
   };
   // x rows of unit u -> this warp's staging area (lane 0 only; VEC: 16-byte rows)
-  auto issue_x = [&](int64_t u) {
-    const int64_t r0 = (u % groups) * ROWS + 2 * warp;
+  auto issue_x = [&](int64_t gx) {  // gx: row group of the unit
+    const int64_t r0 = gx * ROWS + 2 * warp;
     const uint32_t rb = (uint32_t)p.d * 4u;
     const uint32_t bytes = (r0 < p.m ? rb : 0u) + (r0 + 1 < p.m ? rb : 0u);
     mbar_expect_tx(xbar, bytes);
@@ -446,7 +453,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
     if (e_last > e_first) issue_tab(e_first + 1, 1);
   }
   if constexpr (VEC) {
-    if (lane == 0) issue_x(u_lo);
+    if (lane == 0) issue_x(u_lo % groups);
   }
 
   int ti = -1, e_cur = -1;
@@ -454,9 +461,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   const uint2* t_scat = nullptr;
   const float* t_cs = nullptr;
   const uint32_t* t_gc = nullptr;
-  for (int64_t u = u_lo; u < u_hi; ++u) {
-    const int e = (int)(u / groups);
-    const int64_t row0 = (u % groups) * ROWS + 2 * warp;
+  int e = e_first;
+  int64_t g = u_lo - (int64_t)e_first * groups;  // unit u = e * groups + g, advanced incrementally
+  for (int64_t u = u_lo; u < u_hi; ++u, ++g) {
+    if (g == groups) {
+      g = 0;
+      ++e;
+    }
+    const int64_t row0 = g * ROWS + 2 * warp;
     const bool v0 = row0 < p.m, v1 = row0 + 1 < p.m;
     if (e != e_cur) {  // uniform across the CTA
       if (ti >= 0) {
@@ -503,9 +515,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
         const float xa[4] = {a.x, a.y, a.z, a.w}, xb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const uint32_t sg = ((bits >> (4 * j + c)) & 1u) << 31;
-          v[4 * j + c] = make_float2(__uint_as_float(__float_as_uint(xa[c]) ^ sg),
-                                     __uint_as_float(__float_as_uint(xb[c]) ^ sg));
+          // bit (4j+c) of the mask moved to bit 31, XORed into both rows
+          const uint32_t t = bits << (31 - (4 * j + c));
+          v[4 * j + c] = make_float2(__uint_as_float(xor_sign(__float_as_uint(xa[c]), t)),
+                                     __uint_as_float(xor_sign(__float_as_uint(xb[c]), t)));
         }
       }
       if constexpr (VEC) __syncwarp();  // staging reads done before the exchange writes
@@ -553,7 +566,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
       __syncwarp();
       if constexpr (VEC) {
         // next unit's x streams into the (now free) exchange buffer during the epilogue
-        if (lane == 0 && u + 1 < u_hi) issue_x(u + 1);
+        if (lane == 0 && u + 1 < u_hi) issue_x(g + 1 == groups ? 0 : g + 1);
       }
       butterflies2<R, PL, PL>(v);
       // ---- C * scale and the feature epilogue, both rows
