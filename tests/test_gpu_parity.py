@@ -154,13 +154,24 @@ class TestWht:
             ss = float((y.astype(np.float64) ** 2).sum())
             assert abs(ss - float(z[f"n{k}.sumsq"][0])) <= 1e-5 * ss
 
-    def test_cluster_sizes_multi_row(self, cuda):
-        # 2^15..2^18 run as one thread-block cluster per row (DSMEM combine);
-        # 2^19 as column pass + cluster rows
+    def test_large_sizes_multi_row(self, cuda):
+        # 2^15..2^18: one thread-block cluster per row (DSMEM combine);
+        # 2^19, 2^20: column pass + row pass per L2-sized chunk (5 rows = one
+        # partial chunk)
         from paper_1702_08159_b200 import wht_fast_batch
         torch = cuda
-        for k in range(15, 20):
+        for k in range(15, 21):
             x = synthetic.gaussian_rows(5, 1 << k, seed=300 + k)
+            got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+            _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
+
+    def test_large_sizes_many_chunks(self, cuda):
+        # many rows per launch: 2^17 x 150 rows (cluster grid), 2^20 x 19
+        # rows (four 24 MiB chunks, the last one partial)
+        from paper_1702_08159_b200 import wht_fast_batch
+        torch = cuda
+        for k, rows in ((17, 150), (20, 19)):
+            x = synthetic.gaussian_rows(rows, 1 << k, seed=400 + k)
             got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
             _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
 
