@@ -1,17 +1,21 @@
 // K6 tensor-core contractions for the fused config-4 classifier (tcgen05,
 // kind::tf32, 3xTF32 split so the result carries ~fp32 accuracy):
 //
-//   forward : partial logits (128 rows x 16 classes, TMEM) +=
-//             [cos z | sin z] (128 rows x 2*256 features, produced on chip
+//   forward : partial logits (128 rows x 16 classes per row tile, TMEM) +=
+//             [cos z | sin z] (128 rows x 2*128 features, produced on chip
 //             from the L2-resident z tile) * W slice^T
 //   backward: dW tile (128 features = 64 z x {cos, sin}, 16 classes, TMEM) +=
 //             [cos z ; sin z]^T (features x rows) * delta (rows x classes)
 //
-// Features exist only in shared memory.  Producer warps compute sin/cos, split
-// each value x into tf32 hi = x & ~0x1fff and lo = x - hi, and store both in the
+// Features exist only on chip.  Each CTA runs three warp roles: a loader warp
+// streams z (and delta) blocks into shared rings with cp.async, completion
+// signalled on mbarriers; producer warps compute sin/cos, split each value x
+// into tf32 hi = x & ~0x1fff and lo = x - hi and store both in the
 // interleaved K-major layout (umma.cuh); one thread issues A_hi*B_hi +
-// A_hi*B_lo + A_lo*B_hi per K step and commits to an mbarrier that releases
-// the double-buffered stage.  Accumulation is fp32 in TMEM.
+// A_hi*B_lo + A_lo*B_hi per K step and commits to the stage's "empty"
+// mbarrier.  Accumulation is fp32 in TMEM.  The producers never hold
+// outstanding global loads, so the proxy fence before each hand-off (a
+// CTA-scope memory barrier) does not wait on memory latency.
 #include "mck_common.cuh"
 #include "umma.cuh"
 
@@ -19,9 +23,7 @@ namespace mck {
 
 constexpr int kTcM = 128;
 constexpr int kTcN = 16;            // classes padded to the MMA's N
-constexpr int kTcThreads = 256;
 constexpr int kFzCta = 128;         // forward: z values (K = 2 * 128 features) per CTA
-constexpr int kFzStage = 16;        // forward: z values per pipeline stage
 constexpr int kBzCta = 64;          // backward: z values per CTA (M = 128 features)
 constexpr int kBrowStage = 32;      // backward: rows (K) per pipeline stage
 
@@ -35,51 +37,70 @@ __device__ __forceinline__ void sts128(void* p, float a, float b, float c, float
 }
 
 // ---------------------------------------------------------------- forward
+// One CTA per (128-z chunk, group of RTG row tiles of 128 rows): the W slice
+// of the chunk is split into tf32 hi/lo B tiles once and reused for every row
+// tile; partial logits of row tile j accumulate in TMEM columns 16j..16j+15.
+// Warp-specialised pipeline over stages of 8 z x 128 rows:
+//   loader warp  : cp.async (16 B per lane-op) of the stage's z block into a
+//                  kFwdZBuf-deep shared ring, completion signalled on zfull[]
+//                  by cp.async.mbarrier.arrive;
+//   8 producers  : z from the ring, sincos, tf32 hi/lo split, STS in the UMMA
+//                  layout, fence.proxy.async, arrive on full[];
+//   MMA warp     : wait full[], 6 MMAs (3xTF32, cos and sin), commit empty[].
+// The producers hold no outstanding global loads, so their proxy fence (a
+// CTA-scope memory barrier) does not wait on HBM/L2 latency.
+#ifndef MCK_FWD_WARP_ARRIVE
+#define MCK_FWD_WARP_ARRIVE 0
+#endif
+constexpr int kFwdStageZ = 8;                       // z per stage (one K=8 MMA per part)
+constexpr int kFwdBuf = 3;                          // A buffers
+constexpr int kFwdZBuf = 6;                         // z ring stages
+constexpr int kFwdProducers = 256;
+constexpr int kFwdThreads = kFwdProducers + 64;     // + MMA warp + loader warp
+constexpr int kFwdMaxRTG = 8;
+
 struct FwdSmem {
   // B: W slice, rows = 16 classes, K = kFzCta, interleaved; [cos_hi, cos_lo, sin_hi, sin_lo]
   float b[4][kTcN * kFzCta];
-  // A stages: rows = 128, K = kFzStage; [stage][cos_hi, cos_lo, sin_hi, sin_lo]
-  float a[2][4][kTcM * kFzStage];
-  uint64_t bar[2];
+  // A stages: rows = 128, K = 8; [buf][cos_hi, cos_lo, sin_hi, sin_lo]
+  float a[kFwdBuf][4][kTcM * kFwdStageZ];
+  // z ring: [stage][row][8 z]
+  float zr[kFwdZBuf][kTcM * kFwdStageZ];
+  uint64_t full[kFwdBuf], empty[kFwdBuf], zfull[kFwdZBuf], zempty[kFwdZBuf], done;
   uint32_t tslot;
 };
 
-__global__ void __launch_bounds__(kTcThreads, 2)
+__global__ void __launch_bounds__(kFwdThreads, 2)
 k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* __restrict__ w,
-               int64_t F, int C, int64_t col_cos, int64_t col_sin, float* __restrict__ lpart) {
+               int64_t F, int C, int64_t col_cos, int64_t col_sin, int rtg, float* __restrict__ lpart) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   FwdSmem& S = *reinterpret_cast<FwdSmem*>(smraw);
-  const int t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int ks = blockIdx.y;
-  const int64_t r0 = (int64_t)blockIdx.x * kTcM;
   const int64_t z0 = (int64_t)ks * kFzCta;
   const int nz = (int)(n - z0 < kFzCta ? n - z0 : kFzCta);
+  const int64_t rt0 = (int64_t)blockIdx.x * rtg;
+  const int64_t rts = (m + kTcM - 1) / kTcM;
+  const int nrt = (int)(rts - rt0 < rtg ? rts - rt0 : rtg);
+  constexpr int SPR = kFzCta / kFwdStageZ;            // stages per row tile
+  const int stages = nrt * SPR;
+  constexpr int kMmaWarp = kFwdProducers / 32, kLoadWarp = kMmaWarp + 1;
 
-  const int row = t & (kTcM - 1), half = t >> 7;  // 2 threads per row, 8 z each per stage
-  const int64_t gr = r0 + row < m ? r0 + row : m - 1;
-  const float* zr = z + gr * n + z0;
-  // z prefetch ring: stage s+P is requested while stage s is consumed (the z
-  // tile comes from L2/HBM; a 4-deep ring hides its latency)
-  constexpr int SF = kFzCta / kFzStage, P = 4;
-  float4 ring[P][2];
-  auto load_stage = [&](int st, float4 (&dst)[2]) {
-    const int zi = st * kFzStage + half * 8;
-    if (zi + 8 <= nz) {
-      dst[0] = __ldcs(reinterpret_cast<const float4*>(zr + zi));
-      dst[1] = __ldcs(reinterpret_cast<const float4*>(zr + zi + 4));
-    } else {
-      float tmp[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) tmp[j] = zi + j < nz ? __ldcs(zr + zi + j) : 0.f;
-      dst[0] = make_float4(tmp[0], tmp[1], tmp[2], tmp[3]);
-      dst[1] = make_float4(tmp[4], tmp[5], tmp[6], tmp[7]);
+  if (t == 0) {
+    for (int b = 0; b < kFwdBuf; ++b) {
+      mbar_init(&S.full[b], MCK_FWD_WARP_ARRIVE ? kFwdProducers / 32 : kFwdProducers);
+      mbar_init(&S.empty[b], 1);
     }
-  };
-#pragma unroll
-  for (int p = 0; p < P; ++p) load_stage(p, ring[p]);
-
+    for (int b = 0; b < kFwdZBuf; ++b) {
+      mbar_init(&S.zfull[b], 32);
+      mbar_init(&S.zempty[b], kFwdProducers / 32);
+    }
+    mbar_init(&S.done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) umma::tmem_alloc<128>(&S.tslot);
   // W slice -> B tiles (hi/lo), zero for padded classes / z beyond n
-  for (int idx = t; idx < kTcN * kFzCta; idx += kTcThreads) {
+  for (int idx = t; idx < kTcN * kFzCta; idx += blockDim.x) {
     const int c = idx / kFzCta, k = idx % kFzCta;
     float wc = 0.f, wsn = 0.f;
     if (c < C && k < nz) {
@@ -90,108 +111,152 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
     split_tf32(wc, S.b[0][off], S.b[1][off]);
     split_tf32(wsn, S.b[2][off], S.b[3][off]);
   }
-  if (t == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) umma::tmem_alloc<32>(&S.tslot);
+  umma::fence_smem_to_async();
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = S.tslot;
-  constexpr uint32_t idesc = umma::idesc_tf32(kTcM, kTcN);
 
-  // stages beyond nz multiply zero W columns: always run all SF stages
+  if (warp == kLoadWarp) {
+    // ---------------- loader: stage s = 128 rows x 8 z = 256 chunks of 16 B,
+    // 8 per lane; rows clamped into the tile, z beyond n meets zero W columns
+    for (int s = 0; s < stages; ++s) {
+      const int zb = s % kFwdZBuf;
+      if (s >= kFwdZBuf) mbar_wait(&S.zempty[zb], (uint32_t)((s / kFwdZBuf - 1) & 1));
+      const int64_t rbase = (rt0 + s / SPR) * kTcM;
+      const int zi0 = (s % SPR) * kFwdStageZ;
 #pragma unroll
-  for (int s = 0; s < SF; ++s) {
-    const int buf = s & 1;
-    float zv[8] = {ring[s % P][0].x, ring[s % P][0].y, ring[s % P][0].z, ring[s % P][0].w,
-                   ring[s % P][1].x, ring[s % P][1].y, ring[s % P][1].z, ring[s % P][1].w};
-    if (s + P < SF) load_stage(s + P, ring[s % P]);
-    if (s >= 2) mbar_wait(&S.bar[buf], (uint32_t)(((s - 2) >> 1) & 1));
-    const int kb = half * 8;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
+      for (int j = 0; j < 8; ++j) {
+        const int ch = lane + 32 * j, row = ch >> 1, hq = ch & 1;
+        const int64_t r = rbase + row < m ? rbase + row : m - 1;
+        const int zi = zi0 + 4 * hq < nz ? zi0 + 4 * hq : 0;
+        cp_async16(&S.zr[zb][row * kFwdStageZ + 4 * hq], z + r * n + z0 + zi);
+      }
+      cp_async_arrive(&S.zfull[zb]);
+    }
+  } else if (warp < kMmaWarp) {
+    // ---------------- producers: q = z quad of the stage, prow = row
+    const int q = lane >> 4, prow = 16 * warp + (lane & 15);
+    for (int s = 0; s < stages; ++s) {
+      const int zb = s % kFwdZBuf, b = s % kFwdBuf;
+      mbar_wait(&S.zfull[zb], (uint32_t)((s / kFwdZBuf) & 1));
+      const float4 zq = *reinterpret_cast<const float4*>(&S.zr[zb][prow * kFwdStageZ + 4 * q]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.zempty[zb]);
+      if (s >= kFwdBuf) mbar_wait(&S.empty[b], (uint32_t)((s / kFwdBuf - 1) & 1));
+      const float zv[4] = {zq.x, zq.y, zq.z, zq.w};
       float c[4], sn[4], ch[4], cl[4], sh[4], sl[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        __sincosf(zv[4 * q + j], &sn[j], &c[j]);
+        __sincosf(zv[j], &sn[j], &c[j]);
         split_tf32(c[j], ch[j], cl[j]);
         split_tf32(sn[j], sh[j], sl[j]);
       }
-      const uint32_t off = umma::tile_off(row, kb + 4 * q, kTcM);
-      unsigned char* base = reinterpret_cast<unsigned char*>(S.a[buf][0]);
-      constexpr uint32_t AS = kTcM * kFzStage * 4;
+      const uint32_t off = umma::tile_off(prow, 4 * q, kTcM);
+      unsigned char* base = reinterpret_cast<unsigned char*>(S.a[b][0]);
+      constexpr uint32_t AS = kTcM * kFwdStageZ * 4;
       sts128(base + 0 * AS + off, ch[0], ch[1], ch[2], ch[3]);
       sts128(base + 1 * AS + off, cl[0], cl[1], cl[2], cl[3]);
       sts128(base + 2 * AS + off, sh[0], sh[1], sh[2], sh[3]);
       sts128(base + 3 * AS + off, sl[0], sl[1], sl[2], sl[3]);
+      umma::fence_smem_to_async();
+#if MCK_FWD_WARP_ARRIVE
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.full[b]);
+#else
+      mbar_arrive(&S.full[b]);
+#endif
     }
-    umma::fence_smem_to_async();
-    __syncthreads();
-    if (t == 0) {
+  } else if (lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = umma::idesc_tf32(kTcM, kTcN);
+    for (int s = 0; s < stages; ++s) {
+      const int b = s % kFwdBuf, rt = s / SPR, k8 = s % SPR;
+      mbar_wait(&S.full[b], (uint32_t)((s / kFwdBuf) & 1));
       umma::fence_after();
+      const uint32_t acc = tm + (uint32_t)(rt * kTcN);
 #pragma unroll
-      for (int part = 0; part < 2; ++part) {         // cos, sin
-#pragma unroll
-        for (int k0 = 0; k0 < kFzStage; k0 += 8) {
-          const unsigned char* ab = reinterpret_cast<const unsigned char*>(S.a[buf][2 * part]);
-          const unsigned char* al = reinterpret_cast<const unsigned char*>(S.a[buf][2 * part + 1]);
-          const unsigned char* bb = reinterpret_cast<const unsigned char*>(S.b[2 * part]);
-          const unsigned char* bl = reinterpret_cast<const unsigned char*>(S.b[2 * part + 1]);
-          const uint32_t aoff = (k0 / 4) * kTcM * 16;
-          const uint32_t boff = ((s * kFzStage + k0) / 4) * kTcN * 16;
-          const uint64_t dah = umma::smem_desc(ab + aoff, kTcM * 16, 128);
-          const uint64_t dal = umma::smem_desc(al + aoff, kTcM * 16, 128);
-          const uint64_t dbh = umma::smem_desc(bb + boff, kTcN * 16, 128);
-          const uint64_t dbl = umma::smem_desc(bl + boff, kTcN * 16, 128);
-          const uint32_t acc0 = (s > 0 || part > 0 || k0 > 0) ? 1u : 0u;
-          umma::mma_tf32(tm, dah, dbh, idesc, acc0);
-          umma::mma_tf32(tm, dah, dbl, idesc, 1u);
-          umma::mma_tf32(tm, dal, dbh, idesc, 1u);
-        }
+      for (int part = 0; part < 2; ++part) {  // cos, sin
+        const unsigned char* ab = reinterpret_cast<const unsigned char*>(S.a[b][2 * part]);
+        const unsigned char* al = reinterpret_cast<const unsigned char*>(S.a[b][2 * part + 1]);
+        const unsigned char* bb = reinterpret_cast<const unsigned char*>(S.b[2 * part]);
+        const unsigned char* bl = reinterpret_cast<const unsigned char*>(S.b[2 * part + 1]);
+        const uint32_t boff = ((k8 * kFwdStageZ) / 4) * kTcN * 16;
+        const uint64_t dah = umma::smem_desc(ab, kTcM * 16, 128);
+        const uint64_t dal = umma::smem_desc(al, kTcM * 16, 128);
+        const uint64_t dbh = umma::smem_desc(bb + boff, kTcN * 16, 128);
+        const uint64_t dbl = umma::smem_desc(bl + boff, kTcN * 16, 128);
+#ifndef MCK_FWD_MMAS
+#define MCK_FWD_MMAS 3
+#endif
+        if (MCK_FWD_MMAS >= 1) umma::mma_tf32(acc, dah, dbh, idesc, (k8 > 0 || part > 0) ? 1u : 0u);
+        if (MCK_FWD_MMAS >= 2) umma::mma_tf32(acc, dah, dbl, idesc, 1u);
+        if (MCK_FWD_MMAS >= 3) umma::mma_tf32(acc, dal, dbh, idesc, 1u);
       }
-      umma::commit(&S.bar[buf]);
+      umma::commit(&S.empty[b]);
     }
+    umma::commit(&S.done);
   }
-  const int stages = SF;
-  // all MMAs done: the last commit covers every earlier MMA of thread 0
-  if (stages > 0) mbar_wait(&S.bar[(stages - 1) & 1], (uint32_t)(((stages - 1) >> 1) & 1));
-  umma::fence_after();
+  // ---------------- epilogue: TMEM -> partial logits
+  __syncwarp();
   if (warp < 4) {
-    float v[16];
-    umma::tmem_ld16(tm + ((uint32_t)(32 * warp) << 16), v);
-    const int64_t r = r0 + 32 * warp + (t & 31);
-    if (r < m)
-      for (int c = 0; c < C; ++c) lpart[((int64_t)ks * m + r) * C + c] = stages > 0 ? v[c] : 0.f;
+    mbar_wait(&S.done, 0u);
+    umma::fence_after();
+    for (int rt = 0; rt < nrt; ++rt) {
+      float v[16];
+      umma::tmem_ld16(tm + ((uint32_t)(32 * warp) << 16) + (uint32_t)(rt * kTcN), v);
+      const int64_t r = (rt0 + rt) * kTcM + 32 * warp + lane;
+      if (r < m)
+        for (int c = 0; c < C; ++c) lpart[((int64_t)ks * m + r) * C + c] = v[c];
+    }
   }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_free<32>(tm);
+  if (warp == 0) umma::tmem_free<128>(tm);
 }
 
 // ---------------------------------------------------------------- backward
+// One CTA per 64-z slice (M = 128 features: 64 cos, 64 sin), K = all rows in
+// stages of 32 rows; the same warp roles as the forward: a loader warp
+// cp.async-es the stage's z block (32 rows x 64 z) and delta rows into
+// shared rings, 8 producer warps build the A (features) and B (delta) hi/lo
+// tiles, one thread issues the MMAs.
+constexpr int kBwdBuf = 2;
+constexpr int kBwdZBuf = 4;
+constexpr int kBwdProducers = 256;
+constexpr int kBwdThreads = kBwdProducers + 64;
+
 struct BwdSmem {
-  // A stages: rows = 128 features (64 cos, 64 sin), K = 32 rows; [stage][hi, lo]
-  float a[2][2][kTcM * kBrowStage];
-  // B stages: rows = 16 classes, K = 32 rows; [stage][hi, lo]
-  float b[2][2][kTcN * kBrowStage];
-  uint64_t bar[2];
+  // A stages: rows = 128 features (64 cos, 64 sin), K = 32 rows; [buf][hi, lo]
+  float a[kBwdBuf][2][kTcM * kBrowStage];
+  // B stages: rows = 16 classes, K = 32 rows; [buf][hi, lo]
+  float b[kBwdBuf][2][kTcN * kBrowStage];
+  float zr[kBwdZBuf][kBrowStage * kBzCta];      // [stage][row][64 z]
+  float dr[kBwdZBuf][kBrowStage * kTcN];        // [stage][row][C] (C <= 16)
+  uint64_t full[kBwdBuf], empty[kBwdBuf], zfull[kBwdZBuf], zempty[kBwdZBuf], done;
   uint32_t tslot;
 };
 
-__global__ void __launch_bounds__(kTcThreads, 3)
+__global__ void __launch_bounds__(kBwdThreads, 2)
 k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* __restrict__ delta,
                int C, int64_t F, int64_t col_cos, int64_t col_sin, float* dw, float* w, float lr,
                float l2) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   BwdSmem& S = *reinterpret_cast<BwdSmem*>(smraw);
-  const int t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int64_t z0 = (int64_t)blockIdx.x * kBzCta;
+  const int stages = (int)((m + kBrowStage - 1) / kBrowStage);
+  constexpr int kMmaWarp = kBwdProducers / 32, kLoadWarp = kMmaWarp + 1;
   if (t == 0) {
-    mbar_init(&S.bar[0], 1);
-    mbar_init(&S.bar[1], 1);
+    for (int b = 0; b < kBwdBuf; ++b) {
+      mbar_init(&S.full[b], kBwdProducers);
+      mbar_init(&S.empty[b], 1);
+    }
+    for (int b = 0; b < kBwdZBuf; ++b) {
+      mbar_init(&S.zfull[b], 32);
+      mbar_init(&S.zempty[b], kBwdProducers / 32);
+    }
+    mbar_init(&S.done, 1);
     fence_mbar_init();
   }
   if (warp == 0) umma::tmem_alloc<32>(&S.tslot);
@@ -199,76 +264,92 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = S.tslot;
-  constexpr uint32_t idesc = umma::idesc_tf32(kTcM, kTcN);
   constexpr uint32_t AS = kTcM * kBrowStage * 4, BS = kTcN * kBrowStage * 4;
 
-  const int zi = t & 63, q0 = t >> 6;  // A items: (z, row quad q0) and (z, q0 + 4)
-  const bool zok = z0 + zi < n;
-  const int stages = (int)((m + kBrowStage - 1) / kBrowStage);
-  // z prefetch ring (4 stages deep) hides the L2/HBM latency of the z tile
-  constexpr int P = 4;
-  float ring[P][8];
-  auto load_stage = [&](int st, float (&dst)[8]) {
+  if (warp == kLoadWarp) {
+    // ---------------- loader: 32 rows x 64 z (512 chunks of 16 B, 16 per
+    // lane; rows and z clamped into the tile) + the stage's delta rows
+    // (contiguous, 32*C floats; a chunk may run past m*C into the scratch
+    // allocation's 256-byte alignment padding, those values are never used)
+    const int64_t dchunks = (m * C + 3) / 4;
+    for (int s = 0; s < stages; ++s) {
+      const int zb = s % kBwdZBuf;
+      if (s >= kBwdZBuf) mbar_wait(&S.zempty[zb], (uint32_t)((s / kBwdZBuf - 1) & 1));
+      const int64_t rb = (int64_t)s * kBrowStage;
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t r = (int64_t)st * kBrowStage + 4 * (q0 + 4 * h) + j;
-        dst[4 * h + j] = (zok && r < m) ? __ldcs(z + r * n + z0 + zi) : 0.f;
+      for (int j = 0; j < 16; ++j) {
+        const int ch = lane + 32 * j, row = ch >> 4, zq = ch & 15;
+        const int64_t r = rb + row < m ? rb + row : m - 1;
+        const int64_t zi = z0 + 4 * zq < n ? z0 + 4 * zq : 0;
+        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + r * n + zi);
       }
-  };
-#pragma unroll
-  for (int p = 0; p < P; ++p)
-    if (p < stages) load_stage(p, ring[p]);
-  for (int s0 = 0; s0 < stages; s0 += P)
-#pragma unroll
-  for (int u = 0; u < P; ++u) {
-    const int s = s0 + u;
-    if (s >= stages) break;
-    float zv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) zv[j] = ring[u][j];
-    if (s + P < stages) load_stage(s + P, ring[u]);
-    const int buf = s & 1;
-    if (s >= 2) mbar_wait(&S.bar[buf], (uint32_t)(((s - 2) >> 1) & 1));
-    const int64_t rb = (int64_t)s * kBrowStage;
-    unsigned char* A = reinterpret_cast<unsigned char*>(S.a[buf][0]);
-    unsigned char* B = reinterpret_cast<unsigned char*>(S.b[buf][0]);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int q = q0 + 4 * h;
-      float cs[4], sn[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) __sincosf(zv[4 * h + j], &sn[j], &cs[j]);
-      float ch[4], cl[4], sh[4], sl[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        split_tf32(cs[j], ch[j], cl[j]);
-        split_tf32(sn[j], sh[j], sl[j]);
-      }
-      const uint32_t oc = umma::tile_off(zi, 4 * q, kTcM), os = umma::tile_off(64 + zi, 4 * q, kTcM);
-      sts128(A + oc, ch[0], ch[1], ch[2], ch[3]);
-      sts128(A + AS + oc, cl[0], cl[1], cl[2], cl[3]);
-      sts128(A + os, sh[0], sh[1], sh[2], sh[3]);
-      sts128(A + AS + os, sl[0], sl[1], sl[2], sl[3]);
+      const int64_t c0 = rb * C / 4;  // 16-byte chunk index of the stage's first delta
+      for (int j = lane; j < kBrowStage * C / 4; j += 32)
+        if (c0 + j < dchunks) cp_async16(&S.dr[zb][4 * j], delta + 4 * (c0 + j));
+      cp_async_arrive(&S.zfull[zb]);
     }
-    if (t < kTcN * (kBrowStage / 4)) {           // B = delta^T: (class c, row quad q)
-      const int c = t % kTcN, q = t / kTcN;
-      float d[4], dh[4], dl[4];
+  } else if (warp < kMmaWarp) {
+    // ---------------- producers: A items (z zi, row quads q0 and q0 + 4);
+    // B items (class c, row quad q) on threads < 128
+    const int zi = t & 63, q0 = t >> 6;
+    for (int s = 0; s < stages; ++s) {
+      const int zb = s % kBwdZBuf, buf = s % kBwdBuf;
+      const int64_t rb = (int64_t)s * kBrowStage;
+      mbar_wait(&S.zfull[zb], (uint32_t)((s / kBwdZBuf) & 1));
+      float zv[8], d[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t r = rb + 4 * q + j;
-        d[j] = (c < C && r < m) ? delta[r * C + c] : 0.f;
-        split_tf32(d[j], dh[j], dl[j]);
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) zv[4 * h + j] = S.zr[zb][(4 * (q0 + 4 * h) + j) * kBzCta + zi];
+      const int bc = t % kTcN, bq = t / kTcN;
+      if (t < kTcN * (kBrowStage / 4)) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t r = rb + 4 * bq + j;
+          d[j] = (bc < C && r < m) ? S.dr[zb][(4 * bq + j) * C + bc] : 0.f;
+        }
       }
-      const uint32_t ob = umma::tile_off(c, 4 * q, kTcN);
-      sts128(B + ob, dh[0], dh[1], dh[2], dh[3]);
-      sts128(B + BS + ob, dl[0], dl[1], dl[2], dl[3]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.zempty[zb]);
+      if (s >= kBwdBuf) mbar_wait(&S.empty[buf], (uint32_t)((s / kBwdBuf - 1) & 1));
+      unsigned char* A = reinterpret_cast<unsigned char*>(S.a[buf][0]);
+      unsigned char* B = reinterpret_cast<unsigned char*>(S.b[buf][0]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int q = q0 + 4 * h;
+        float cs[4], sn[4], ch[4], cl[4], sh[4], sl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __sincosf(zv[4 * h + j], &sn[j], &cs[j]);
+          split_tf32(cs[j], ch[j], cl[j]);
+          split_tf32(sn[j], sh[j], sl[j]);
+        }
+        const uint32_t oc = umma::tile_off(zi, 4 * q, kTcM), os = umma::tile_off(64 + zi, 4 * q, kTcM);
+        sts128(A + oc, ch[0], ch[1], ch[2], ch[3]);
+        sts128(A + AS + oc, cl[0], cl[1], cl[2], cl[3]);
+        sts128(A + os, sh[0], sh[1], sh[2], sh[3]);
+        sts128(A + AS + os, sl[0], sl[1], sl[2], sl[3]);
+      }
+      if (t < kTcN * (kBrowStage / 4)) {  // B = delta^T: (class c, row quad q); zero rows >= m
+        float dh[4], dl[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(d[j], dh[j], dl[j]);
+        const uint32_t ob = umma::tile_off(bc, 4 * bq, kTcN);
+        sts128(B + ob, dh[0], dh[1], dh[2], dh[3]);
+        sts128(B + BS + ob, dl[0], dl[1], dl[2], dl[3]);
+      }
+      umma::fence_smem_to_async();
+      mbar_arrive(&S.full[buf]);
     }
-    umma::fence_smem_to_async();
-    __syncthreads();
-    if (t == 0) {
+  } else if (lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = umma::idesc_tf32(kTcM, kTcN);
+    for (int s = 0; s < stages; ++s) {
+      const int buf = s % kBwdBuf;
+      mbar_wait(&S.full[buf], (uint32_t)((s / kBwdBuf) & 1));
       umma::fence_after();
+      const unsigned char* A = reinterpret_cast<const unsigned char*>(S.a[buf][0]);
+      const unsigned char* B = reinterpret_cast<const unsigned char*>(S.b[buf][0]);
 #pragma unroll
       for (int k0 = 0; k0 < kBrowStage; k0 += 8) {
         const uint32_t aoff = (k0 / 4) * kTcM * 16, boff = (k0 / 4) * kTcN * 16;
@@ -280,15 +361,17 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
         umma::mma_tf32(tm, dah, dbl, idesc, 1u);
         umma::mma_tf32(tm, dal, dbh, idesc, 1u);
       }
-      umma::commit(&S.bar[buf]);
+      umma::commit(&S.empty[buf]);
     }
+    umma::commit(&S.done);
   }
-  if (stages > 0) mbar_wait(&S.bar[(stages - 1) & 1], (uint32_t)(((stages - 1) >> 1) & 1));
-  umma::fence_after();
+  __syncwarp();
   if (warp < 4) {
+    if (stages > 0) mbar_wait(&S.done, 0u);
+    umma::fence_after();
     float v[16];
     umma::tmem_ld16(tm + ((uint32_t)(32 * warp) << 16), v);
-    const int f = 32 * warp + (t & 31);   // feature row of the tile
+    const int f = 32 * warp + lane;   // feature row of the tile
     const int zz = f & 63;
     if (z0 + zz < n) {
       const int64_t col = (f < 64 ? col_cos : col_sin) + z0 + zz;
@@ -318,8 +401,16 @@ int fused_fwd_tc(const float* z, int64_t m, int64_t n, const float* w, int64_t F
                                             (int)smem), "fwd tc smem"));
     init = true;
   }
-  dim3 grid((unsigned)((m + kTcM - 1) / kTcM), (unsigned)((n + kFzCta - 1) / kFzCta));
-  k_fused_fwd_tc<<<grid, kTcThreads, smem, st>>>(z, m, n, w, F, C, col_cos, col_sin, lpart);
+  const int64_t KS = (n + kFzCta - 1) / kFzCta, RT = (m + kTcM - 1) / kTcM;
+  // row tiles per CTA: enough CTAs for one wave of 2 per SM, W slice reused
+  int64_t per = 296 / KS;
+  if (per < 1) per = 1;
+  int64_t rtg = (RT + per - 1) / per;
+  if (rtg > kFwdMaxRTG) rtg = kFwdMaxRTG;
+  if (rtg < 1) rtg = 1;
+  dim3 grid((unsigned)((RT + rtg - 1) / rtg), (unsigned)KS);
+  k_fused_fwd_tc<<<grid, kFwdThreads, smem, st>>>(z, m, n, w, F, C, col_cos, col_sin,
+                                                         (int)rtg, lpart);
   return check_launch("k_fused_fwd_tc");
 }
 
@@ -335,7 +426,7 @@ int fused_bwd_tc(const float* z, int64_t m, int64_t n, const float* delta, int C
     init = true;
   }
   const unsigned grid = (unsigned)((n + kBzCta - 1) / kBzCta);
-  k_fused_bwd_tc<<<grid, kTcThreads, smem, st>>>(z, m, n, delta, C, F, col_cos, col_sin, dw, w,
+  k_fused_bwd_tc<<<grid, kBwdThreads, smem, st>>>(z, m, n, delta, C, F, col_cos, col_sin, dw, w,
                                                  lr, l2);
   return check_launch("k_fused_bwd_tc");
 }

@@ -34,12 +34,14 @@ def _case(cuda, spec, m, seed, tc=True):
 
 
 @pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
-@pytest.mark.parametrize("which", ["small", "c4"])
+@pytest.mark.parametrize("which", ["small", "ragged", "c4"])
 def test_fused_forward_backward(cuda, which, tc):
     import paper_1702_08159_b200 as P
     torch = cuda
     if which == "small":
         spec, m = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3), 96
+    elif which == "ragged":  # m*C not a multiple of 4, partial row tile / stage
+        spec, m = P.FeatureMapSpec(300, 2, P.RBF(1.0), 8), 37
     else:
         spec, m = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4), 8
     fc, x, y, phi = _case(cuda, spec, m, 11, tc)
