@@ -155,10 +155,17 @@ struct FFParams {
 // flight while iteration it computes.
 template <class C>
 constexpr int ff_min_blocks() {
-  return C::R >= 64 ? 2 : (C::T * ff_rows_per_cta<C>() <= 256 ? 3 : 1);
+  return C::R >= 64 ? 2 : (C::T * ff_rows_per_cta<C>() <= 256 ? 3 : 2);
 }
+// x kept in registers across the E blocks: small rows only (n = 16384 runs
+// 512-thread rows at two CTAs per SM and re-reads x per block)
+template <class C>
+constexpr bool ff_xreg() { return C::R <= 32 && C::LOGN < 14; }
+#ifndef MCK_C14_LOGR
+#define MCK_C14_LOGR 5
+#endif
 
-template <class C, bool FEAT, bool FOLD, bool VEC, bool XREG = (C::R <= 32)>
+template <class C, bool FEAT, bool FOLD, bool VEC, bool XREG = ff_xreg<C>()>
 __global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>(), ff_min_blocks<C>())
 k_fastfood(FFParams p) {
   constexpr int R = C::R, T = C::T, N = C::N, W = (R + 31) / 32;
@@ -809,7 +816,7 @@ int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st,
     case 11: return prepare_cfg<RowCfg<11, 5>>(tv, st);
     case 12: return prepare_cfg<RowCfg<12, 5>>(tv, st);
     case 13: return prepare_cfg<RowCfg<13, 5>>(tv, st);
-    case 14: return prepare_cfg<RowCfg<14, 6>>(tv, st);
+    case 14: return prepare_cfg<RowCfg<14, MCK_C14_LOGR>>(tv, st);
     default: return MCK_OK;  // fused kernel not available; parity path only
   }
 }
@@ -937,7 +944,7 @@ int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream
     case 11: return launch_ff_cfg<RowCfg<11, 5>>(p, feat, fold, vec, st);
     case 12: return launch_ff_cfg<RowCfg<12, 5>>(p, feat, fold, vec, st);
     case 13: return launch_ff_cfg<RowCfg<13, 5>>(p, feat, fold, vec, st);
-    case 14: return launch_ff_cfg<RowCfg<14, 6>>(p, feat, fold, vec, st);
+    case 14: return launch_ff_cfg<RowCfg<14, MCK_C14_LOGR>>(p, feat, fold, vec, st);
     default: return fail_value("unsupported padded_dim 2^%d", logn);
   }
 }
