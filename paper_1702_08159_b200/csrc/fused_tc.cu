@@ -38,35 +38,33 @@ __device__ __forceinline__ void sts128(void* p, float a, float b, float c, float
 
 // ---------------------------------------------------------------- forward
 // One CTA per (128-z chunk, group of RTG row tiles of 128 rows): the W slice
-// of the chunk is split into tf32 hi/lo B tiles once and reused for every row
-// tile; partial logits of row tile j accumulate in TMEM columns 16j..16j+15.
-// Warp-specialised pipeline over stages of 8 z x 128 rows:
-//   loader warp  : cp.async (16 B per lane-op) of the stage's z block into a
-//                  kFwdZBuf-deep shared ring, completion signalled on zfull[]
-//                  by cp.async.mbarrier.arrive;
-//   8 producers  : z from the ring, sincos, tf32 hi/lo split, STS in the UMMA
-//                  layout, fence.proxy.async, arrive on full[];
-//   MMA warp     : wait full[], 6 MMAs (3xTF32, cos and sin), commit empty[].
-// The producers hold no outstanding global loads, so their proxy fence (a
-// CTA-scope memory barrier) does not wait on HBM/L2 latency.
-#ifndef MCK_FWD_WARP_ARRIVE
-#define MCK_FWD_WARP_ARRIVE 0
-#endif
-constexpr int kFwdStageZ = 8;                       // z per stage (one K=8 MMA per part)
-constexpr int kFwdBuf = 3;                          // A buffers
-constexpr int kFwdZBuf = 6;                         // z ring stages
+// of the chunk is split into tf32 hi/lo B tiles (shared memory) once and
+// reused for every row tile; partial logits of row tile j accumulate in TMEM
+// columns 16j..16j+15.  Pipeline over stages of 16 z x 128 rows:
+//   8 producer warps: each thread streams its own 8 z of the stage (one row,
+//     two z quads) into a private kFwdZD-deep shared ring with cp.async
+//     (cp.async.wait_group, no cross-thread hand-off), computes sincos and the
+//     tf32 hi/lo split, and writes the four A tiles (cos/sin x hi/lo; row =
+//     TMEM lane, k = column) into the stage's TMEM buffer with tcgen05.st,
+//     then arrives on full[];
+//   MMA thread: wait full[], 12 MMAs with A from TMEM (3xTF32, cos and sin,
+//     two K = 8 steps), commit to empty[].
+// The A operand never touches shared memory.
+constexpr int kFwdStageZ = 16;                      // z per stage (two K=8 MMAs per part)
+constexpr int kFwdBuf = 3;                          // A buffers (TMEM)
+constexpr int kFwdZD = 8;                           // z prefetch depth (stages)
 constexpr int kFwdProducers = 256;
-constexpr int kFwdThreads = kFwdProducers + 64;     // + MMA warp + loader warp
-constexpr int kFwdMaxRTG = 8;
+constexpr int kFwdThreads = kFwdProducers + 32;     // + MMA warp
+constexpr int kFwdMaxRTG = 4;                       // accumulators: TMEM columns 0..63
+constexpr uint32_t kFwdAcol = 64;                   // A buffers: columns 64 + 64 b + 16 sub + k
+constexpr uint32_t kFwdTmemCols = 256;
 
 struct FwdSmem {
   // B: W slice, rows = 16 classes, K = kFzCta, interleaved; [cos_hi, cos_lo, sin_hi, sin_lo]
   float b[4][kTcN * kFzCta];
-  // A stages: rows = 128, K = 8; [buf][cos_hi, cos_lo, sin_hi, sin_lo]
-  float a[kFwdBuf][4][kTcM * kFwdStageZ];
-  // z ring: [stage][row][8 z]
-  float zr[kFwdZBuf][kTcM * kFwdStageZ];
-  uint64_t full[kFwdBuf], empty[kFwdBuf], zfull[kFwdZBuf], zempty[kFwdZBuf], done;
+  // per-thread z ring: [stage slot][quad j][thread] float4
+  float4 zr[kFwdZD][2][kFwdProducers];
+  uint64_t full[kFwdBuf], empty[kFwdBuf], done;
   uint32_t tslot;
 };
 
@@ -84,21 +82,34 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   const int nrt = (int)(rts - rt0 < rtg ? rts - rt0 : rtg);
   constexpr int SPR = kFzCta / kFwdStageZ;            // stages per row tile
   const int stages = nrt * SPR;
-  constexpr int kMmaWarp = kFwdProducers / 32, kLoadWarp = kMmaWarp + 1;
+  constexpr int kMmaWarp = kFwdProducers / 32;
 
   if (t == 0) {
     for (int b = 0; b < kFwdBuf; ++b) {
-      mbar_init(&S.full[b], MCK_FWD_WARP_ARRIVE ? kFwdProducers / 32 : kFwdProducers);
+      mbar_init(&S.full[b], kFwdProducers);
       mbar_init(&S.empty[b], 1);
-    }
-    for (int b = 0; b < kFwdZBuf; ++b) {
-      mbar_init(&S.zfull[b], 32);
-      mbar_init(&S.zempty[b], kFwdProducers / 32);
     }
     mbar_init(&S.done, 1);
     fence_mbar_init();
   }
-  if (warp == 0) umma::tmem_alloc<128>(&S.tslot);
+  if (warp == 0) umma::tmem_alloc<kFwdTmemCols>(&S.tslot);
+  // producer mapping: warp w writes TMEM lanes 32*(w%4).. (rows) and the
+  // columns of z quads q, q+1 with q = 2*(w/4)
+  const int q = 2 * (warp >> 2), prow = 32 * (warp & 3) + lane;
+  // rows clamped into the tile, z beyond n meets zero W columns
+  auto issue = [&](int s) {
+    if (s < stages) {
+      const int64_t r = (rt0 + s / SPR) * kTcM + prow;
+      const float* zp = z + (r < m ? r : m - 1) * n + z0;
+      const int zi = (s % SPR) * kFwdStageZ + 4 * q;
+      const int slot = s % kFwdZD;
+      cp_async16(&S.zr[slot][0][t], zp + (zi < nz ? zi : 0));
+      cp_async16(&S.zr[slot][1][t], zp + (zi + 4 < nz ? zi + 4 : 0));
+    }
+    cp_async_commit();  // one group per stage (possibly empty)
+  };
+  if (warp < kMmaWarp)
+    for (int d = 0; d < kFwdZD; ++d) issue(d);
   // W slice -> B tiles (hi/lo), zero for padded classes / z beyond n
   for (int idx = t; idx < kTcN * kFzCta; idx += blockDim.x) {
     const int c = idx / kFzCta, k = idx % kFzCta;
@@ -116,57 +127,39 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = S.tslot;
-
-  if (warp == kLoadWarp) {
-    // ---------------- loader: stage s = 128 rows x 8 z = 256 chunks of 16 B,
-    // 8 per lane; rows clamped into the tile, z beyond n meets zero W columns
+  if (warp < kMmaWarp) {
+    // ---------------- producers
+    const uint32_t lane_base = tm + ((uint32_t)(32 * (warp & 3)) << 16);
     for (int s = 0; s < stages; ++s) {
-      const int zb = s % kFwdZBuf;
-      if (s >= kFwdZBuf) mbar_wait(&S.zempty[zb], (uint32_t)((s / kFwdZBuf - 1) & 1));
-      const int64_t rbase = (rt0 + s / SPR) * kTcM;
-      const int zi0 = (s % SPR) * kFwdStageZ;
+      const int b = s % kFwdBuf, slot = s % kFwdZD;
+      cp_async_wait<kFwdZD - 1>();  // stage s (this thread's own copies) landed
+      const float4 za = S.zr[slot][0][t], zc = S.zr[slot][1][t];
+      const float zv[8] = {za.x, za.y, za.z, za.w, zc.x, zc.y, zc.z, zc.w};
+      float c[8], sn[8], ch[8], cl[8], sh[8], sl[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int ch = lane + 32 * j, row = ch >> 1, hq = ch & 1;
-        const int64_t r = rbase + row < m ? rbase + row : m - 1;
-        const int zi = zi0 + 4 * hq < nz ? zi0 + 4 * hq : 0;
-        cp_async16(&S.zr[zb][row * kFwdStageZ + 4 * hq], z + r * n + z0 + zi);
-      }
-      cp_async_arrive(&S.zfull[zb]);
-    }
-  } else if (warp < kMmaWarp) {
-    // ---------------- producers: q = z quad of the stage, prow = row
-    const int q = lane >> 4, prow = 16 * warp + (lane & 15);
-    for (int s = 0; s < stages; ++s) {
-      const int zb = s % kFwdZBuf, b = s % kFwdBuf;
-      mbar_wait(&S.zfull[zb], (uint32_t)((s / kFwdZBuf) & 1));
-      const float4 zq = *reinterpret_cast<const float4*>(&S.zr[zb][prow * kFwdStageZ + 4 * q]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.zempty[zb]);
-      if (s >= kFwdBuf) mbar_wait(&S.empty[b], (uint32_t)((s / kFwdBuf - 1) & 1));
-      const float zv[4] = {zq.x, zq.y, zq.z, zq.w};
-      float c[4], sn[4], ch[4], cl[4], sh[4], sl[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
         __sincosf(zv[j], &sn[j], &c[j]);
         split_tf32(c[j], ch[j], cl[j]);
         split_tf32(sn[j], sh[j], sl[j]);
       }
-      const uint32_t off = umma::tile_off(prow, 4 * q, kTcM);
-      unsigned char* base = reinterpret_cast<unsigned char*>(S.a[b][0]);
-      constexpr uint32_t AS = kTcM * kFwdStageZ * 4;
-      sts128(base + 0 * AS + off, ch[0], ch[1], ch[2], ch[3]);
-      sts128(base + 1 * AS + off, cl[0], cl[1], cl[2], cl[3]);
-      sts128(base + 2 * AS + off, sh[0], sh[1], sh[2], sh[3]);
-      sts128(base + 3 * AS + off, sl[0], sl[1], sl[2], sl[3]);
-      umma::fence_smem_to_async();
-#if MCK_FWD_WARP_ARRIVE
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.full[b]);
-#else
+      issue(s + kFwdZD);  // the slot's values are consumed above
+      if (s >= kFwdBuf) {
+        mbar_wait(&S.empty[b], (uint32_t)((s / kFwdBuf - 1) & 1));
+        umma::fence_after();
+      }
+      const uint32_t col = lane_base + kFwdAcol + (uint32_t)(64 * b + 4 * q);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        umma::tmem_st4(col + 4 * h + 0, ch[4 * h], ch[4 * h + 1], ch[4 * h + 2], ch[4 * h + 3]);
+        umma::tmem_st4(col + 4 * h + 16, cl[4 * h], cl[4 * h + 1], cl[4 * h + 2], cl[4 * h + 3]);
+        umma::tmem_st4(col + 4 * h + 32, sh[4 * h], sh[4 * h + 1], sh[4 * h + 2], sh[4 * h + 3]);
+        umma::tmem_st4(col + 4 * h + 48, sl[4 * h], sl[4 * h + 1], sl[4 * h + 2], sl[4 * h + 3]);
+      }
+      umma::tmem_wait_st();
+      umma::fence_before();
       mbar_arrive(&S.full[b]);
-#endif
     }
+    cp_async_wait<0>();
   } else if (lane == 0) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = umma::idesc_tf32(kTcM, kTcN);
@@ -175,44 +168,51 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
       mbar_wait(&S.full[b], (uint32_t)((s / kFwdBuf) & 1));
       umma::fence_after();
       const uint32_t acc = tm + (uint32_t)(rt * kTcN);
+      const uint32_t abuf = tm + kFwdAcol + (uint32_t)(64 * b);
 #pragma unroll
       for (int part = 0; part < 2; ++part) {  // cos, sin
-        const unsigned char* ab = reinterpret_cast<const unsigned char*>(S.a[b][2 * part]);
-        const unsigned char* al = reinterpret_cast<const unsigned char*>(S.a[b][2 * part + 1]);
-        const unsigned char* bb = reinterpret_cast<const unsigned char*>(S.b[2 * part]);
-        const unsigned char* bl = reinterpret_cast<const unsigned char*>(S.b[2 * part + 1]);
-        const uint32_t boff = ((k8 * kFwdStageZ) / 4) * kTcN * 16;
-        const uint64_t dah = umma::smem_desc(ab, kTcM * 16, 128);
-        const uint64_t dal = umma::smem_desc(al, kTcM * 16, 128);
-        const uint64_t dbh = umma::smem_desc(bb + boff, kTcN * 16, 128);
-        const uint64_t dbl = umma::smem_desc(bl + boff, kTcN * 16, 128);
-#ifndef MCK_FWD_MMAS
-#define MCK_FWD_MMAS 3
-#endif
-        if (MCK_FWD_MMAS >= 1) umma::mma_tf32(acc, dah, dbh, idesc, (k8 > 0 || part > 0) ? 1u : 0u);
-        if (MCK_FWD_MMAS >= 2) umma::mma_tf32(acc, dah, dbl, idesc, 1u);
-        if (MCK_FWD_MMAS >= 3) umma::mma_tf32(acc, dal, dbh, idesc, 1u);
+#pragma unroll
+        for (int kk = 0; kk < kFwdStageZ; kk += 8) {
+          const unsigned char* bb = reinterpret_cast<const unsigned char*>(S.b[2 * part]);
+          const unsigned char* bl = reinterpret_cast<const unsigned char*>(S.b[2 * part + 1]);
+          const uint32_t boff = ((k8 * kFwdStageZ + kk) / 4) * kTcN * 16;
+          const uint64_t dbh = umma::smem_desc(bb + boff, kTcN * 16, 128);
+          const uint64_t dbl = umma::smem_desc(bl + boff, kTcN * 16, 128);
+          const uint32_t ah = abuf + (uint32_t)(32 * part + kk), al = ah + 16;
+          umma::mma_tf32_ts(acc, ah, dbh, idesc, (k8 > 0 || part > 0 || kk > 0) ? 1u : 0u);
+          umma::mma_tf32_ts(acc, ah, dbl, idesc, 1u);
+          umma::mma_tf32_ts(acc, al, dbh, idesc, 1u);
+        }
       }
       umma::commit(&S.empty[b]);
     }
     umma::commit(&S.done);
   }
-  // ---------------- epilogue: TMEM -> partial logits
+  // ---------------- epilogue: TMEM -> partial logits.  Rows rt0*128 ..
+  // of chunk ks are one contiguous [rows][C] block of lpart: stage it in
+  // shared memory (the z ring is idle now) and store it coalesced.
   __syncwarp();
+  float* stage_out = reinterpret_cast<float*>(&S.zr[0][0][0]);  // nrt*128*C <= 4*128*16 floats
   if (warp < 4) {
     mbar_wait(&S.done, 0u);
     umma::fence_after();
     for (int rt = 0; rt < nrt; ++rt) {
       float v[16];
       umma::tmem_ld16(tm + ((uint32_t)(32 * warp) << 16) + (uint32_t)(rt * kTcN), v);
-      const int64_t r = (rt0 + rt) * kTcM + 32 * warp + lane;
-      if (r < m)
-        for (int c = 0; c < C; ++c) lpart[((int64_t)ks * m + r) * C + c] = v[c];
+      float* o = stage_out + (rt * kTcM + 32 * warp + lane) * C;
+      for (int c = 0; c < C; ++c) o[c] = v[c];
     }
+  }
+  __syncthreads();
+  {
+    const int64_t r0 = rt0 * kTcM;
+    const int64_t nrows = m - r0 < (int64_t)nrt * kTcM ? m - r0 : (int64_t)nrt * kTcM;
+    float* dst = lpart + ((int64_t)ks * m + r0) * C;
+    for (int64_t i = t; i < nrows * C; i += blockDim.x) dst[i] = stage_out[i];
   }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_free<128>(tm);
+  if (warp == 0) umma::tmem_free<kFwdTmemCols>(tm);
 }
 
 // ---------------------------------------------------------------- backward
