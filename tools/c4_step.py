@@ -8,9 +8,10 @@ from paper_1702_08159_b200.large_scale import FusedClassifier
 
 spec = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4)
 tc = "--cuda-cores" not in sys.argv
-fc = FusedClassifier(spec, 10, 1024, tensor_cores=tc)
-x = torch.randn((1024, 16384), device="cuda")
-y = torch.randint(0, 10, (1024,), device="cuda", dtype=torch.int32)
+M = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--rows=")), 1024))
+fc = FusedClassifier(spec, 10, M, tensor_cores=tc)
+x = torch.randn((M, 16384), device="cuda")
+y = torch.randint(0, 10, (M,), device="cuda", dtype=torch.int32)
 for _ in range(2):
     fc.step(x, y, m_total=8192, lr=0.01)
 torch.cuda.synchronize()
