@@ -196,6 +196,8 @@ k_fastfood(FFParams p) {
     if constexpr (ff_colored<C>())
       bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)e * (N / 4), N, b);
   };
+  pdl_wait();
+  pdl_trigger();
   if (STAGED) {
     if (threadIdx.x == 0) {
       mbar_init(bar, 1);
@@ -426,6 +428,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
   const int64_t units = groups * p.E;
   const int64_t u_lo = units * blockIdx.x / gridDim.x, u_hi = units * (blockIdx.x + 1) / gridDim.x;
+  pdl_wait();
+  pdl_trigger();
   if (u_lo >= u_hi) return;
   const int e_first = (int)(u_lo / groups), e_last = (int)((u_hi - 1) / groups);
   auto issue_tab = [&](int e, int slot) {  // thread 0 only
@@ -651,8 +655,7 @@ int launch_ff_pair(const FFParams& p, cudaStream_t st) {
   const int64_t items = (p.m + ROWS - 1) / ROWS * p.E;
   int64_t grid = (int64_t)sms * occ;
   if (grid > items) grid = items;
-  kern<<<(unsigned)grid, kPairWarps * 32, smem, st>>>(p);
-  return check_launch("k_fastfood_pair");
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kPairWarps * 32), smem, st, "k_fastfood_pair", p);
 }
 
 // ---------------------------------------------------------------- parity variant
@@ -840,8 +843,7 @@ int launch_ff(const FFParams& p, cudaStream_t st) {
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
   int64_t grid = (int64_t)sms * occ;
   if (grid > groups) grid = groups;
-  kern<<<(unsigned)grid, C::T * ROWS, smem, st>>>(p);
-  return check_launch("k_fastfood");
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(C::T * ROWS), smem, st, "k_fastfood", p);
 }
 
 template <class C>

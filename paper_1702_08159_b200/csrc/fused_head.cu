@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(kFoldWarps * 32)
 k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C, double* logits,
              int first) {
   __shared__ double part[kFoldWarps][32];
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t mc = m * C;
   const int64_t t = (int64_t)blockIdx.x * 32 + lane;
@@ -308,9 +310,8 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                                                      D + (int64_t)e * n, fs.lpart);
       return check_launch("k_fused_fwd");
     }));
-    k_fused_fold<<<(unsigned)((m * C + 31) / 32), kFoldWarps * 32, 0, st>>>(
-        fs.lpart, KS, m, C, fs.logits, e == 0 ? 1 : 0);
-    MCK_TRY(check_launch("k_fused_fold"));
+    MCK_TRY(launch_pdl(k_fused_fold, dim3((unsigned)((m * C + 31) / 32)), dim3(kFoldWarps * 32), 0, st,
+                       "k_fused_fold", (const float*)fs.lpart, KS, m, (int)C, fs.logits, e == 0 ? 1 : 0));
   }
   if (logits_out)
     MCK_TRY(check_cuda(cudaMemcpyAsync(logits_out, fs.logits, m * C * 8, cudaMemcpyDeviceToDevice, st),

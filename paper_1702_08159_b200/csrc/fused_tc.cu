@@ -108,9 +108,8 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
     }
     cp_async_commit();  // one group per stage (possibly empty)
   };
-  if (warp < kMmaWarp)
-    for (int d = 0; d < kFwdZD; ++d) issue(d);
-  // W slice -> B tiles (hi/lo), zero for padded classes / z beyond n
+  // W slice -> B tiles (hi/lo), zero for padded classes / z beyond n (W is
+  // not written by the z producer this kernel follows: read before pdl_wait)
   for (int idx = t; idx < kTcN * kFzCta; idx += blockDim.x) {
     const int c = idx / kFzCta, k = idx % kFzCta;
     float wc = 0.f, wsn = 0.f;
@@ -122,6 +121,10 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
     split_tf32(wc, S.b[0][off], S.b[1][off]);
     split_tf32(wsn, S.b[2][off], S.b[3][off]);
   }
+  pdl_wait();  // z tile complete
+  pdl_trigger();
+  if (warp < kMmaWarp)
+    for (int d = 0; d < kFwdZD; ++d) issue(d);
   umma::fence_smem_to_async();
   umma::fence_before();
   __syncthreads();
@@ -247,6 +250,8 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   const int64_t z0 = (int64_t)blockIdx.x * kBzCta;
   const int stages = (int)((m + kBrowStage - 1) / kBrowStage);
   constexpr int kMmaWarp = kBwdProducers / 32, kLoadWarp = kMmaWarp + 1;
+  pdl_wait();
+  pdl_trigger();
   if (t == 0) {
     for (int b = 0; b < kBwdBuf; ++b) {
       mbar_init(&S.full[b], kBwdProducers);
@@ -409,9 +414,8 @@ int fused_fwd_tc(const float* z, int64_t m, int64_t n, const float* w, int64_t F
   if (rtg > kFwdMaxRTG) rtg = kFwdMaxRTG;
   if (rtg < 1) rtg = 1;
   dim3 grid((unsigned)((RT + rtg - 1) / rtg), (unsigned)KS);
-  k_fused_fwd_tc<<<grid, kFwdThreads, smem, st>>>(z, m, n, w, F, C, col_cos, col_sin,
-                                                         (int)rtg, lpart);
-  return check_launch("k_fused_fwd_tc");
+  return launch_pdl(k_fused_fwd_tc, grid, dim3(kFwdThreads), smem, st, "k_fused_fwd_tc", z, m, n, w,
+                    F, C, col_cos, col_sin, (int)rtg, lpart);
 }
 
 int fused_bwd_tc(const float* z, int64_t m, int64_t n, const float* delta, int C, int64_t F,
@@ -426,9 +430,8 @@ int fused_bwd_tc(const float* z, int64_t m, int64_t n, const float* delta, int C
     init = true;
   }
   const unsigned grid = (unsigned)((n + kBzCta - 1) / kBzCta);
-  k_fused_bwd_tc<<<grid, kBwdThreads, smem, st>>>(z, m, n, delta, C, F, col_cos, col_sin, dw, w,
-                                                 lr, l2);
-  return check_launch("k_fused_bwd_tc");
+  return launch_pdl(k_fused_bwd_tc, dim3(grid), dim3(kBwdThreads), smem, st, "k_fused_bwd_tc", z, m, n,
+                    delta, C, F, col_cos, col_sin, dw, w, lr, l2);
 }
 
 int64_t fused_tc_ksplits(int64_t n) { return (n + kFzCta - 1) / kFzCta; }

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/mckernel_b200.h"
@@ -28,6 +29,37 @@ int check_launch(const char* what);
     int _rc = (expr);                                   \
     if (_rc != MCK_OK) return _rc;                      \
   } while (0)
+
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: kernels of the hot loops are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs may
+// become resident while its predecessor in the stream drains.  Every such
+// kernel calls pdl_wait() before it touches memory a predecessor may write
+// or read (griddepcontrol.wait returns once the predecessor grid completed
+// and its writes are visible), then pdl_trigger() so that its own successor
+// can be scheduled; code before pdl_wait() touches only constant inputs and
+// on-chip state.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               const char* what, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), what));
+  return check_launch(what);
+}
 
 // ---------------------------------------------------------------- hashing
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
