@@ -220,18 +220,21 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
 
 // ---------------------------------------------------------------- backward
 // One CTA per 64-z slice (M = 128 features: 64 cos, 64 sin), K = all rows in
-// stages of 32 rows; the same warp roles as the forward: a loader warp
-// cp.async-es the stage's z block (32 rows x 64 z) and delta rows into
-// shared rings, 8 producer warps build the A (features) and B (delta) hi/lo
-// tiles, one thread issues the MMAs.
-constexpr int kBwdBuf = 2;
+// stages of 32 rows.  A cp.async loader warp streams the stage's z block
+// (32 rows x 64 z) and delta rows into shared rings; 8 producer warps write
+// the A operand (feature = TMEM lane, row = column; tf32 hi/lo) with
+// tcgen05.st -- warp w owns lanes 32*(w%4).. (cos for the first 64 features,
+// sin for the rest) and rows 16*(w/4)..+15 of the stage -- and 4 of them
+// build the small B tiles (delta^T hi/lo) in shared memory; one thread
+// issues 12 MMAs per stage with A from TMEM.
+constexpr int kBwdBuf = 3;
 constexpr int kBwdZBuf = 4;
 constexpr int kBwdProducers = 256;
 constexpr int kBwdThreads = kBwdProducers + 64;
+constexpr uint32_t kBwdAcol = 32;                 // A buffers: columns 32 + 64 b + {0: hi, 32: lo} + k
+constexpr uint32_t kBwdTmemCols = 256;
 
 struct BwdSmem {
-  // A stages: rows = 128 features (64 cos, 64 sin), K = 32 rows; [buf][hi, lo]
-  float a[kBwdBuf][2][kTcM * kBrowStage];
   // B stages: rows = 16 classes, K = 32 rows; [buf][hi, lo]
   float b[kBwdBuf][2][kTcN * kBrowStage];
   float zr[kBwdZBuf][kBrowStage * kBzCta];      // [stage][row][64 z]
@@ -264,12 +267,12 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
     mbar_init(&S.done, 1);
     fence_mbar_init();
   }
-  if (warp == 0) umma::tmem_alloc<32>(&S.tslot);
+  if (warp == 0) umma::tmem_alloc<kBwdTmemCols>(&S.tslot);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t tm = S.tslot;
-  constexpr uint32_t AS = kTcM * kBrowStage * 4, BS = kTcN * kBrowStage * 4;
+  constexpr uint32_t BS = kTcN * kBrowStage * 4;
 
   if (warp == kLoadWarp) {
     // ---------------- loader: 32 rows x 64 z (512 chunks of 16 B, 16 per
@@ -294,19 +297,23 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
       cp_async_arrive(&S.zfull[zb]);
     }
   } else if (warp < kMmaWarp) {
-    // ---------------- producers: A items (z zi, row quads q0 and q0 + 4);
-    // B items (class c, row quad q) on threads < 128
-    const int zi = t & 63, q0 = t >> 6;
+    // ---------------- producers
+    const int lq = warp & 3, rh = warp >> 2;
+    const int f = 32 * lq + lane, zi = f & 63;
+    const bool is_cos = lq < 2;
+    const uint32_t lane_base = tm + ((uint32_t)(32 * lq) << 16);
+    const int bc = t % kTcN, bq = t / kTcN;   // B items on threads < 128
     for (int s = 0; s < stages; ++s) {
       const int zb = s % kBwdZBuf, buf = s % kBwdBuf;
       const int64_t rb = (int64_t)s * kBrowStage;
       mbar_wait(&S.zfull[zb], (uint32_t)((s / kBwdZBuf) & 1));
-      float zv[8], d[4];
+      float hi[16], lo[16], d[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) zv[4 * h + j] = S.zr[zb][(4 * (q0 + 4 * h) + j) * kBzCta + zi];
-      const int bc = t % kTcN, bq = t / kTcN;
+      for (int j = 0; j < 16; ++j) {
+        const float zz = S.zr[zb][(16 * rh + j) * kBzCta + zi];
+        const float v = is_cos ? __cosf(zz) : __sinf(zz);
+        split_tf32(v, hi[j], lo[j]);
+      }
       if (t < kTcN * (kBrowStage / 4)) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -316,34 +323,25 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.zempty[zb]);
-      if (s >= kBwdBuf) mbar_wait(&S.empty[buf], (uint32_t)((s / kBwdBuf - 1) & 1));
-      unsigned char* A = reinterpret_cast<unsigned char*>(S.a[buf][0]);
-      unsigned char* B = reinterpret_cast<unsigned char*>(S.b[buf][0]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int q = q0 + 4 * h;
-        float cs[4], sn[4], ch[4], cl[4], sh[4], sl[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          __sincosf(zv[4 * h + j], &sn[j], &cs[j]);
-          split_tf32(cs[j], ch[j], cl[j]);
-          split_tf32(sn[j], sh[j], sl[j]);
-        }
-        const uint32_t oc = umma::tile_off(zi, 4 * q, kTcM), os = umma::tile_off(64 + zi, 4 * q, kTcM);
-        sts128(A + oc, ch[0], ch[1], ch[2], ch[3]);
-        sts128(A + AS + oc, cl[0], cl[1], cl[2], cl[3]);
-        sts128(A + os, sh[0], sh[1], sh[2], sh[3]);
-        sts128(A + AS + os, sl[0], sl[1], sl[2], sl[3]);
+      if (s >= kBwdBuf) {
+        mbar_wait(&S.empty[buf], (uint32_t)((s / kBwdBuf - 1) & 1));
+        umma::fence_after();
       }
+      const uint32_t col = lane_base + kBwdAcol + (uint32_t)(64 * buf + 16 * rh);
+      umma::tmem_st16(col, hi);
+      umma::tmem_st16(col + 32, lo);
       if (t < kTcN * (kBrowStage / 4)) {  // B = delta^T: (class c, row quad q); zero rows >= m
+        unsigned char* B = reinterpret_cast<unsigned char*>(S.b[buf][0]);
         float dh[4], dl[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) split_tf32(d[j], dh[j], dl[j]);
         const uint32_t ob = umma::tile_off(bc, 4 * bq, kTcN);
         sts128(B + ob, dh[0], dh[1], dh[2], dh[3]);
         sts128(B + BS + ob, dl[0], dl[1], dl[2], dl[3]);
+        umma::fence_smem_to_async();
       }
-      umma::fence_smem_to_async();
+      umma::tmem_wait_st();
+      umma::fence_before();
       mbar_arrive(&S.full[buf]);
     }
   } else if (lane == 0) {
@@ -353,18 +351,17 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
       const int buf = s % kBwdBuf;
       mbar_wait(&S.full[buf], (uint32_t)((s / kBwdBuf) & 1));
       umma::fence_after();
-      const unsigned char* A = reinterpret_cast<const unsigned char*>(S.a[buf][0]);
       const unsigned char* B = reinterpret_cast<const unsigned char*>(S.b[buf][0]);
+      const uint32_t abuf = tm + kBwdAcol + (uint32_t)(64 * buf);
 #pragma unroll
       for (int k0 = 0; k0 < kBrowStage; k0 += 8) {
-        const uint32_t aoff = (k0 / 4) * kTcM * 16, boff = (k0 / 4) * kTcN * 16;
-        const uint64_t dah = umma::smem_desc(A + aoff, kTcM * 16, 128);
-        const uint64_t dal = umma::smem_desc(A + AS + aoff, kTcM * 16, 128);
+        const uint32_t boff = (k0 / 4) * kTcN * 16;
         const uint64_t dbh = umma::smem_desc(B + boff, kTcN * 16, 128);
         const uint64_t dbl = umma::smem_desc(B + BS + boff, kTcN * 16, 128);
-        umma::mma_tf32(tm, dah, dbh, idesc, (s > 0 || k0 > 0) ? 1u : 0u);
-        umma::mma_tf32(tm, dah, dbl, idesc, 1u);
-        umma::mma_tf32(tm, dal, dbh, idesc, 1u);
+        const uint32_t ah = abuf + (uint32_t)k0, al = ah + 32;
+        umma::mma_tf32_ts(tm, ah, dbh, idesc, (s > 0 || k0 > 0) ? 1u : 0u);
+        umma::mma_tf32_ts(tm, ah, dbl, idesc, 1u);
+        umma::mma_tf32_ts(tm, al, dbh, idesc, 1u);
       }
       umma::commit(&S.empty[buf]);
     }
@@ -393,7 +390,7 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   }
   umma::fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_free<32>(tm);
+  if (warp == 0) umma::tmem_free<kBwdTmemCols>(tm);
 }
 
 int fused_fwd_tc(const float* z, int64_t m, int64_t n, const float* w, int64_t F, int C,
