@@ -25,6 +25,7 @@
 #include "async_copy.cuh"
 #include "perm_color.cuh"
 
+#include <cstring>
 #include <vector>
 
 namespace mck {
@@ -140,6 +141,8 @@ struct FFParams {
   const uint2* scat;
   const float* cs;
   const uint32_t* gcol;
+  const uint16_t* soff;
+  const float* ggath;
   float scale;
   float norm;
   float* out;
@@ -396,9 +399,14 @@ __device__ __forceinline__ void lds2(const float2* s, uint32_t tpart, float2 (&v
   for (int k = 0; k < R; ++k) v[k] = base[pad2(deposit_bits((uint32_t)k, P))];
 }
 
+// two-row kernel table slot: soff u16[N] | ggath f32[N] | cs f32[N] | bmask | gcol u8[N]
+template <class C>
+constexpr int pair_tab_bytes() { return C::N * 11 + bm_stride<C>() * 4; }
+template <class C>
+constexpr int pair_tab_slot() { return (pair_tab_bytes<C>() + 127) & ~127; }
 template <class C>
 constexpr size_t ff_pair_smem_bytes() {
-  return 128 + 2 * (size_t)tab_slot<C>() + (size_t)kPairWarps * kPairRowFloat2 * 8;
+  return 128 + 2 * (size_t)pair_tab_slot<C>() + (size_t)kPairWarps * kPairRowFloat2 * 8;
 }
 
 template <bool FEAT, bool FOLD, bool VEC>
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   using C = RowCfg<10, 5>;
   constexpr int R = C::R, T = C::T, N = C::N;
   constexpr int ROWS = 2 * kPairWarps;
-  constexpr int SLOT = tab_slot<C>();
+  constexpr int SLOT = pair_tab_slot<C>();
   constexpr uint32_t PL = C::PL, P0 = C::mid_regs(0);
   static_assert(C::NMID == 1 && T == 32, "pair kernel layout");
   static_assert(2 * N * 4 <= kPairRowFloat2 * 8, "x staging fits the exchange buffer");
@@ -436,11 +444,13 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
     const int eg = p.e0 + e;
     unsigned char* dst = tabs + slot * SLOT;
     uint64_t* b = bar + slot;
-    mbar_expect_tx(b, tab_bytes<C>());
-    bulk_g2s(dst, p.scat + (int64_t)eg * N, N * 8, b);
-    bulk_g2s(dst + N * 8, p.cs + (int64_t)eg * N, N * 4, b);
-    bulk_g2s(dst + N * 12, p.bmask + (int64_t)eg * bm_stride<C>(), bm_stride<C>() * 4, b);
-    bulk_g2s(dst + N * 12 + bm_stride<C>() * 4, p.gcol + (int64_t)eg * (N / 4), N, b);
+    // slot: soff u16[N] | ggath f32[N] | cs f32[N] | bmask | gcol u8[N]
+    mbar_expect_tx(b, pair_tab_bytes<C>());
+    bulk_g2s(dst, p.soff + (int64_t)eg * N, N * 2, b);
+    bulk_g2s(dst + N * 2, p.ggath + (int64_t)eg * N, N * 4, b);
+    bulk_g2s(dst + N * 6, p.cs + (int64_t)eg * N, N * 4, b);
+    bulk_g2s(dst + N * 10, p.bmask + (int64_t)eg * bm_stride<C>(), bm_stride<C>() * 4, b);
+    bulk_g2s(dst + N * 10 + bm_stride<C>() * 4, p.gcol + (int64_t)eg * (N / 4), N, b);
   };
   auto src_row = [&](int64_t r) -> const float* {
     return p.x + (p.rows ? (int64_t)p.rows[r] : r) * p.ldx;
@@ -469,7 +479,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
 
   int ti = -1, e_cur = -1;
   uint32_t xph = 0, bits = 0;
-  const uint2* t_scat = nullptr;
+  const uint4* t_soff = nullptr;
+  const float4* t_gg = nullptr;
   const float* t_cs = nullptr;
   const uint32_t* t_gc = nullptr;
   int e = e_first;
@@ -490,10 +501,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
       e_cur = e;
       mbar_wait(bar + (ti & 1), (uint32_t)((ti >> 1) & 1));
       const unsigned char* tb = tabs + (ti & 1) * SLOT;
-      t_scat = reinterpret_cast<const uint2*>(tb);
-      t_cs = reinterpret_cast<const float*>(tb + N * 8);
-      bits = reinterpret_cast<const uint32_t*>(tb + N * 12)[lane];
-      t_gc = reinterpret_cast<const uint32_t*>(tb + N * 12 + bm_stride<C>() * 4);
+      t_soff = reinterpret_cast<const uint4*>(tb);
+      t_gg = reinterpret_cast<const float4*>(tb + N * 2);
+      t_cs = reinterpret_cast<const float*>(tb + N * 6);
+      bits = reinterpret_cast<const uint32_t*>(tb + N * 10)[lane];
+      t_gc = reinterpret_cast<const uint32_t*>(tb + N * 10 + bm_stride<C>() * 4);
     }
     float* const orow0 = p.out + (v0 ? row0 : 0) * p.ldo;
     float* const orow1 = p.out + (v1 ? row0 + 1 : 0) * p.ldo;
@@ -541,19 +553,16 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
       lds2<R, P0>(s, tp_0, v);
       __syncwarp();
       butterflies2<R, P0, P0>(v);
-      // ---- Pi and G: scatter (coloured 8-byte slots), gather
+      // ---- Pi and G: scatter (coloured 8-byte slots, 16-bit byte offsets),
+      // gather, then y[p] = z1[perm[p]] * g[p] (the reference's fp32 product)
 #pragma unroll
       for (int k0 = 0; k0 < R; k0 += 8) {
-        uint2 a[8];
+        const uint4 o = t_soff[(k0 / 8) * T + lane];
+        const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + lane];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float2 w = v[k0 + q];
-          const float g = __uint_as_float(a[q].y);
-          mul_pk(w.x, w.y, g, g);
-          *reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + a[q].x) = w;
-        }
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float2*>(reinterpret_cast<char*>(s) + ((ow[q / 2] >> (16 * (q % 2))) & 0xffffu)) =
+              v[k0 + q];
       }
       __syncwarp();
       {
@@ -562,9 +571,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
 #pragma unroll
         for (int k4 = 0; k4 < R / 4; ++k4) {
           const uint32_t cw = t_gc[k4 * T + lane];
+          const float4 g4 = t_gg[k4 * T + lane];
+          const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            v[4 * k4 + q] = *reinterpret_cast<const float2*>(gb + (4 * k4 + q) * 256 + ((cw >> (8 * q)) & 0xffu));
+          for (int q = 0; q < 4; ++q) {
+            float2 w = *reinterpret_cast<const float2*>(gb + (4 * k4 + q) * 256 + ((cw >> (8 * q)) & 0xffu));
+            mul_pk(w.x, w.y, gg[q], gg[q]);
+            v[4 * k4 + q] = w;
+          }
         }
       }
       __syncwarp();
@@ -751,6 +765,8 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
     }
   std::vector<uint2> scat((size_t)E * N);
   std::vector<uint32_t> gcol((size_t)E * N / 4, 0u);
+  std::vector<uint16_t> soff(PAIR ? (size_t)E * N : 0);
+  std::vector<float> ggath(PAIR ? (size_t)E * N : 0);
   std::vector<int32_t> left(N), right(N);
   std::vector<uint8_t> col(N);
   for (int e = 0; e < E; ++e) {
@@ -767,7 +783,23 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
           make_uint2((uint32_t)ES * ((uint32_t)GW * (uint32_t)ggrp[p] + col[j]), gbits[(size_t)e * N + p]);
       const int k = gpos[p] / T, t = gpos[p] % T;
       gcol[(size_t)e * (N / 4) + (k / 4) * T + t] |= ((uint32_t)ES * col[j]) << (8 * (k % 4));
+      if constexpr (PAIR) {
+        const uint32_t off = (uint32_t)ES * ((uint32_t)GW * (uint32_t)ggrp[p] + col[j]);
+        if (off > 0xffffu) return fail_value("internal: scatter offset exceeds 16 bits");
+        const int sk = spos[j] / T, st_ = spos[j] % T;
+        soff[(size_t)e * N + ((size_t)(sk / 8) * T + st_) * 8 + sk % 8] = (uint16_t)off;
+        uint32_t gb = gbits[(size_t)e * N + p];
+        float gf;
+        memcpy(&gf, &gb, 4);
+        ggath[(size_t)e * N + ((size_t)(k / 4) * T + t) * 4 + k % 4] = gf;
+      }
     }
+  }
+  if constexpr (PAIR) {
+    MCK_TRY(check_cuda(cudaMemcpyAsync(tv.soff, soff.data(), soff.size() * 2,
+                                       cudaMemcpyHostToDevice, st), "soff H2D"));
+    MCK_TRY(check_cuda(cudaMemcpyAsync(tv.ggath, ggath.data(), ggath.size() * 4,
+                                       cudaMemcpyHostToDevice, st), "ggath H2D"));
   }
   MCK_TRY(check_cuda(cudaMemcpyAsync(tv.scat, scat.data(), scat.size() * 8,
                                      cudaMemcpyHostToDevice, st), "scat H2D"));
@@ -903,6 +935,7 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
   FFParams p{};
   p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
   p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs; p.gcol = tv.gcol;
+  p.soff = tv.soff; p.ggath = tv.ggath;
   p.scale = scale; p.norm = norm; p.out = out; p.ldo = ldo; p.E = tv.E; p.D = D;
   return launch_by_logn(p, logn, feat, fold, st);
 }
@@ -924,6 +957,7 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   FFParams p{};
   p.x = x; p.m = m; p.ldx = ldx; p.d = d; p.rows = rows;
   p.bmask = tv.bmask; p.scat = tv.scat; p.cs = tv.cs; p.gcol = tv.gcol;
+  p.soff = tv.soff; p.ggath = tv.ggath;
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
   p.keep_l2 = 1;

@@ -24,6 +24,8 @@ struct TablesView {
   uint32_t* bmask;   // [E][words][T]  sign bits in layout-L register order
   uint2* scat;       // [E][R][T]      {smem byte offset of element j's slot, bits of g[perm^-1[j]]}
   uint32_t* gcol;    // [E][R/4][T]    gather slot colours (4 bytes per word; n >= 1024)
+  uint16_t* soff;    // [E][R/8][T][8] scatter slot byte offsets (n = 1024 two-row kernel)
+  float* ggath;      // [E][R/4][T][4] g in the gather layout (n = 1024 two-row kernel)
   int32_t* flag;     // validation flag
 };
 
@@ -52,6 +54,8 @@ inline int64_t tables_layout(int64_t n, int32_t E, char* base, TablesView* tv) {
   v.bmask = (uint32_t*)take(((en + 31) / 32 + (int64_t)E * 64) * 4);
   v.scat = (uint2*)take(en * 8);
   v.gcol = (uint32_t*)take(en);
+  v.soff = (uint16_t*)take(en * 2);
+  v.ggath = (float*)take(en * 4);
   v.flag = (int32_t*)take(16);
   if (tv) *tv = v;
   return off;
