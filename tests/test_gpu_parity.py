@@ -428,3 +428,24 @@ class TestHead:
             assert abs(rec.test_acc - acc) <= 0.002          # 0.2 percentage points
             assert abs(rec.train_loss - loss) <= 1e-4 * abs(loss) + 1e-7
         np.testing.assert_allclose(model.b.cpu().numpy(), g["b"], rtol=1e-3, atol=1e-6)
+
+
+class TestHostStreaming:
+    def test_feature_map_to_host_matches_device(self, cuda):
+        # the bench's e2e path: pinned host rows -> H2D / expansion / D2H on
+        # three streams, double-buffered, several batches and a ragged tail
+        import paper_1702_08159_b200 as P
+        from paper_1702_08159_b200.streaming import HostStreamer, feature_map_to_host
+        torch = cuda
+        spec = P.FeatureMapSpec(784, 4, P.RBFMatern(2.0, 5), 42)
+        blocks = P.build_blocks(spec)
+        x = torch.from_numpy(synthetic.image_rows(650, 784, 5)).pin_memory()
+        want = P.feature_map_batch(spec, blocks, x.cuda()).cpu()
+        got = feature_map_to_host(spec, blocks, x, batch_rows=128)
+        assert torch.equal(got, want)
+        hs = HostStreamer(spec, blocks, 100)
+        out = torch.empty_like(got).pin_memory()
+        for _ in range(2):  # reuse of the staging buffers across calls
+            out.zero_()
+            hs.run(x, out)
+            assert torch.equal(out, want)
