@@ -164,9 +164,6 @@ constexpr int ff_min_blocks() {
 // 512-thread rows at two CTAs per SM and re-reads x per block)
 template <class C>
 constexpr bool ff_xreg() { return C::R <= 32 && C::LOGN < 14; }
-#ifndef MCK_C14_LOGR
-#define MCK_C14_LOGR 5
-#endif
 
 template <class C, bool FEAT, bool FOLD, bool VEC, bool XREG = ff_xreg<C>()>
 __global__ void __launch_bounds__(C::T * ff_rows_per_cta<C>(), ff_min_blocks<C>())
@@ -350,15 +347,7 @@ __device__ __forceinline__ uint32_t xor_sign(uint32_t x, uint32_t t) {
   return r;
 }
 
-// Feature stores.  MCK_FF_STORE_CS=1 marks them streaming (evict-first), which
-// keeps the re-read inputs and tables resident in L2 (A/B switch).
-#ifndef MCK_FF_STORE_CS
-#define MCK_FF_STORE_CS 0
-#endif
-__device__ __forceinline__ void st_out(float4* p, float4 v) {
-  if constexpr (MCK_FF_STORE_CS) __stcs(p, v);
-  else *p = v;
-}
+__device__ __forceinline__ void st_out(float4* p, float4 v) { *p = v; }
 
 // ---------------------------------------------------------------- two rows per thread
 // n = 1024.  Each warp owns TWO rows; register k holds the pair (row0[i],
@@ -851,7 +840,7 @@ int prepare_tables(const TablesView& tv, float scale, int fold, cudaStream_t st,
     case 11: return prepare_cfg<RowCfg<11, 5>>(tv, st);
     case 12: return prepare_cfg<RowCfg<12, 5>>(tv, st);
     case 13: return prepare_cfg<RowCfg<13, 5>>(tv, st);
-    case 14: return prepare_cfg<RowCfg<14, MCK_C14_LOGR>>(tv, st);
+    case 14: return prepare_cfg<RowCfg<14, 5>>(tv, st);
     default: return MCK_OK;  // fused kernel not available; parity path only
   }
 }
@@ -980,7 +969,7 @@ int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream
     case 11: return launch_ff_cfg<RowCfg<11, 5>>(p, feat, fold, vec, st);
     case 12: return launch_ff_cfg<RowCfg<12, 5>>(p, feat, fold, vec, st);
     case 13: return launch_ff_cfg<RowCfg<13, 5>>(p, feat, fold, vec, st);
-    case 14: return launch_ff_cfg<RowCfg<14, MCK_C14_LOGR>>(p, feat, fold, vec, st);
+    case 14: return launch_ff_cfg<RowCfg<14, 5>>(p, feat, fold, vec, st);
     default: return fail_value("unsupported padded_dim 2^%d", logn);
   }
 }
