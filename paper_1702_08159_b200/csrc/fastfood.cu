@@ -182,7 +182,16 @@ k_fastfood(FFParams p) {
   constexpr uint32_t P0 = C::mid_regs(0);
 
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
-  const int64_t my_groups = groups > blockIdx.x ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // XREG: groups strided over the CTAs, all E blocks per group (x read once).
+  // Otherwise (n = 16384): balanced contiguous ranges of (group, block)
+  // items, so that a launch over several blocks fills every wave.
+  static_assert(XREG || !STAGED, "item ranges assume per-item table reads");
+  const int64_t items = groups * p.E;
+  const int64_t it_lo = XREG ? 0 : items * blockIdx.x / gridDim.x;
+  const int64_t it_hi = XREG ? 0 : items * (blockIdx.x + 1) / gridDim.x;
+  const int64_t g_first = XREG ? 0 : it_lo / p.E;
+  const int64_t my_groups = XREG ? (groups > blockIdx.x ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0)
+                                 : (it_hi > it_lo ? (it_hi - 1) / p.E - g_first + 1 : 0);
   const int64_t total_it = my_groups * p.E;
 
   auto issue = [&](int64_t it) {  // thread 0 only
@@ -209,8 +218,11 @@ k_fastfood(FFParams p) {
   }
 
   for (int64_t gi = 0; gi < my_groups; ++gi) {
-    const int64_t row = (blockIdx.x + gi * gridDim.x) * ROWS + gid;
+    const int64_t grp = XREG ? blockIdx.x + gi * gridDim.x : g_first + gi;
+    const int64_t row = grp * ROWS + gid;
     const bool valid = row < p.m;
+    const int e_lo = XREG ? 0 : (int)(grp == it_lo / p.E ? it_lo % p.E : 0);
+    const int e_hi = XREG ? p.E : (int)(grp == (it_hi - 1) / p.E ? (it_hi - 1) % p.E + 1 : p.E);
     // ---- input row, layout L, zero padded (kept in registers for all E blocks)
     const float* xp = p.x + (valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0) * p.ldx;
     auto load_x = [&](float (&dst)[R]) {
@@ -233,7 +245,7 @@ k_fastfood(FFParams p) {
     if constexpr (XREG) load_x(xr);
     float* orow = p.out + (valid ? row : 0) * p.ldo;
 
-    for (int e = 0; e < p.E; ++e) {
+    for (int e = e_lo; e < e_hi; ++e) {
       const int64_t it = gi * p.E + e;
       const uint2* t_scat;
       const float* t_cs;
@@ -862,8 +874,9 @@ int launch_ff(const FFParams& p, cudaStream_t st) {
     if (occ < 1) occ = 1;
   }
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
+  const int64_t work = ff_xreg<C>() ? groups : groups * p.E;
   int64_t grid = (int64_t)sms * occ;
-  if (grid > groups) grid = groups;
+  if (grid > work) grid = work;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(C::T * ROWS), smem, st, "k_fastfood", p);
 }
 

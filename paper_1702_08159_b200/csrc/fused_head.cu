@@ -2,25 +2,25 @@
 // (BASELINE config 4: d = n = 16384, E = 32, 2^20 features per row, 10
 // classes).  Features are never written to HBM:
 //
-//   for each block e:   k_fastfood (z of block e only, fastfood_z_blocks)
-//                         -> z tile (m x n fp32) in an L2-resident scratch
-//                       k_fused_fwd: cos/sin computed on the fly from z,
-//                         contracted with the W slice of block e (shared
-//                         memory) into per-chunk partial logits
-//                       k_fused_fold: partial logits -> float64 logits
-//                         (fixed order: blocks ascending, fixed tree over chunks)
+//   for each pair of blocks: k_fastfood (z of the two blocks only,
+//                         fastfood_z_blocks) -> z tile (m x 2n fp32, scratch)
+//     for each block e:   k_fused_fwd_tc: cos/sin computed on chip from z,
+//                         contracted with the W slice of block e on the
+//                         tensor cores into per-chunk partial logits
+//                         k_fused_fold: partial logits -> float64 logits
+//                         (fixed order: blocks ascending, chunks in order)
 //   softmax / loss / delta (classifier.cu, k_head_softmax)
-//   for each block e:   k_fastfood again (recompute z; cheaper than storing
-//                         2^20 features per row)
-//                       k_fused_bwd: dW slice of block e = delta^T [cos z | sin z]
-//                         with cos/sin on the fly, row-split partials
-//                       k_fused_dw_finish: reduce splits (fixed order) and
-//                         either write dW (multi-GPU: all-reduced by the
-//                         caller) or apply the SGD update in place.
+//   for each pair of blocks: k_fastfood again (recompute z; cheaper than
+//                         storing 2^20 features per row)
+//     for each block e:   k_fused_bwd_tc: dW slice of block e = delta^T
+//                         [cos z | sin z] with cos/sin on chip, written or
+//                         applied as the SGD update in place.
+// (k_fused_fwd / k_fused_bwd / k_fused_dw_finish: the CUDA-core cross-check
+// variant of the two contractions.)
 //
 // W is float32 (C x 2nE; 41.9 MB at config 4, the all-reduce payload named in
 // SURVEY.md section 2.1), logits and loss float64, contraction accumulators
-// float32 within a chunk of 512 features.
+// float32 within a chunk of features.
 #include <type_traits>
 
 #include "mck_common.cuh"
@@ -36,6 +36,11 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
                              double* rowloss, int32_t* rowhit, cudaStream_t st);
 
 constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
+// Blocks whose z the producer computes per launch: (row, block) items fill
+// the producer's waves better (1,024 rows x 2 blocks over 296 CTA slots: 6.9
+// of 7 waves instead of 3.5 of 4) and halve its launches; the tile
+// (m x kFusedZBlocks*n) is read back by the contractions from L2/HBM.
+constexpr int kFusedZBlocks = 2;
 int64_t fused_tc_ksplits(int64_t n);  // fused_tc.cu
 constexpr int kFwarps = 8;
 constexpr int kFrowsPerWarp = 4;
@@ -47,7 +52,7 @@ constexpr int kBrowChunk = 128;
 constexpr int kFusedMaxClasses = 16;
 
 struct FusedScratch {
-  float* z;          // [m][n]
+  float* z;          // [m][kFusedZBlocks * n]
   float* lpart;      // [KS][m][C]     partial logits of the current block
   double* logits;    // [m][C]
   double* rowloss;   // [m]
@@ -73,7 +78,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
   const int64_t KS_cc = (n + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(n);
   const int64_t KS = KS_cc > KS_tc ? KS_cc : KS_tc;   // partial-logit chunks of either variant
   FusedScratch s{};
-  s.z = (float*)take(m * n * 4);
+  s.z = (float*)take(m * n * kFusedZBlocks * 4);
   s.lpart = (float*)take(KS * m * C * 4);
   s.logits = (double*)take(m * C * 8);
   s.rowloss = (double*)take(m * 8);
@@ -88,7 +93,8 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
 // lpart[ks][r][c] = sum_{i in chunk ks} cos(z[r][i]) W[c][e n + i] + sin(z[r][i]) W[c][D + e n + i]
 template <int NC>
 __global__ void __launch_bounds__(kFwarps * 32) k_fused_fwd(const float* __restrict__ z, int64_t m,
-                                                            int64_t n, const float* __restrict__ w,
+                                                            int64_t n, int64_t ldz,
+                                                            const float* __restrict__ w,
                                                             int64_t F, int64_t col_cos,
                                                             int64_t col_sin, float* __restrict__ lpart) {
   __shared__ __align__(16) float wc[NC][kFzChunk];
@@ -111,7 +117,7 @@ __global__ void __launch_bounds__(kFwarps * 32) k_fused_fwd(const float* __restr
     for (int c = 0; c < NC; ++c) acc[q][c] = 0.f;
   const float* zr[kFrowsPerWarp];
 #pragma unroll
-  for (int q = 0; q < kFrowsPerWarp; ++q) zr[q] = z + (r0 + q < m ? r0 + q : m - 1) * n + i0;
+  for (int q = 0; q < kFrowsPerWarp; ++q) zr[q] = z + (r0 + q < m ? r0 + q : m - 1) * ldz + i0;
   for (int i = lane; i < ni; i += 32) {
     float cs[kFrowsPerWarp], sn[kFrowsPerWarp];
 #pragma unroll
@@ -180,7 +186,8 @@ __global__ void k_to_f32(const double* a, float* b, int64_t n) {
 // dwpart[rs][c][n + i]  = sum_{r in split} delta[r][c] sin(z[r][i])
 template <int NC>
 __global__ void __launch_bounds__(kBthreads) k_fused_bwd(const float* __restrict__ z, int64_t m,
-                                                         int64_t n, const float* __restrict__ delta,
+                                                         int64_t n, int64_t ldz,
+                                                         const float* __restrict__ delta,
                                                          int64_t rows_per_split,
                                                          float* __restrict__ dwpart) {
   __shared__ float sd[kBrowChunk][NC];
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kBthreads) k_fused_bwd(const float* __restrict
     __syncthreads();
 #pragma unroll 2
     for (int rr = 0; rr < nr; ++rr) {
-      const float* zr = z + (r0 + rr) * n;
+      const float* zr = z + (r0 + rr) * ldz;
       float cs[kBzPerThread], sn[kBzPerThread];
 #pragma unroll
       for (int j = 0; j < kBzPerThread; ++j) {
@@ -283,9 +290,9 @@ static int dispatch_nc(int C, Fn fn) {
 
 int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t C) { return fused_layout(m, n, C, nullptr, nullptr); }
 
-int fused_fwd_tc(const float*, int64_t, int64_t, const float*, int64_t, int, int64_t, int64_t,
+int fused_fwd_tc(const float*, int64_t, int64_t, int64_t, const float*, int64_t, int, int64_t, int64_t,
                  float*, cudaStream_t);
-int fused_bwd_tc(const float*, int64_t, int64_t, const float*, int, int64_t, int64_t, int64_t,
+int fused_bwd_tc(const float*, int64_t, int64_t, int64_t, const float*, int, int64_t, int64_t, int64_t,
                  float*, float*, float, float, cudaStream_t);
 int64_t fused_tc_ksplits(int64_t n);
 
@@ -299,14 +306,19 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
   FusedScratch fs;
   fused_layout(m, n, C, (char*)scratch, &fs);
   const int64_t KS = cuda_cores ? (n + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(n);
+  const int64_t ldz = n * kFusedZBlocks;
   for (int32_t e = 0; e < E; ++e) {
-    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
+    const int32_t zb = e % kFusedZBlocks;  // block's column slot in the z tile
+    if (zb == 0)
+      MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e,
+                                (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks), fs.z, ldz, st));
+    const float* zt = fs.z + (int64_t)zb * n;
     if (!cuda_cores)
-      MCK_TRY(fused_fwd_tc(fs.z, m, n, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+      MCK_TRY(fused_fwd_tc(zt, m, n, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
     else MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
-      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(fs.z, m, n, w, F, (int64_t)e * n,
+      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(zt, m, n, ldz, w, F, (int64_t)e * n,
                                                      D + (int64_t)e * n, fs.lpart);
       return check_launch("k_fused_fwd");
     }));
@@ -333,17 +345,22 @@ int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x
   const int64_t rps = (m + RS - 1) / RS;
   k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
   MCK_TRY(check_launch("k_to_f32"));
+  const int64_t ldz = n * kFusedZBlocks;
   for (int32_t e = 0; e < E; ++e) {
-    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, 1, fs.z, n, st));
+    const int32_t zb = e % kFusedZBlocks;
+    if (zb == 0)
+      MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e,
+                                (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks), fs.z, ldz, st));
+    const float* zt = fs.z + (int64_t)zb * n;
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_tc(fs.z, m, n, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw, w,
+      MCK_TRY(fused_bwd_tc(zt, m, n, ldz, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw, w,
                            (float)lr, (float)l2, st));
       continue;
     }
     MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((n + kBz - 1) / kBz), (unsigned)RS);
-      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(fs.z, m, n, fs.delta32, rps, fs.dwpart);
+      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(zt, m, n, ldz, fs.delta32, rps, fs.dwpart);
       return check_launch("k_fused_bwd");
     }));
     int64_t grid = ((int64_t)C * 2 * n + 255) / 256;

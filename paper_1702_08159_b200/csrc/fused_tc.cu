@@ -69,8 +69,9 @@ struct FwdSmem {
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2)
-k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* __restrict__ w,
-               int64_t F, int C, int64_t col_cos, int64_t col_sin, int rtg, float* __restrict__ lpart) {
+k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
+               const float* __restrict__ w, int64_t F, int C, int64_t col_cos, int64_t col_sin, int rtg,
+               float* __restrict__ lpart) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   FwdSmem& S = *reinterpret_cast<FwdSmem*>(smraw);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -100,7 +101,7 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   auto issue = [&](int s) {
     if (s < stages) {
       const int64_t r = (rt0 + s / SPR) * kTcM + prow;
-      const float* zp = z + (r < m ? r : m - 1) * n + z0;
+      const float* zp = z + (r < m ? r : m - 1) * ldz + z0;
       const int zi = (s % SPR) * kFwdStageZ + 4 * q;
       const int slot = s % kFwdZD;
       cp_async16(&S.zr[slot][0][t], zp + (zi < nz ? zi : 0));
@@ -244,9 +245,9 @@ struct BwdSmem {
 };
 
 __global__ void __launch_bounds__(kBwdThreads, 2)
-k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* __restrict__ delta,
-               int C, int64_t F, int64_t col_cos, int64_t col_sin, float* dw, float* w, float lr,
-               float l2) {
+k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
+               const float* __restrict__ delta, int C, int64_t F, int64_t col_cos, int64_t col_sin,
+               float* dw, float* w, float lr, float l2) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   BwdSmem& S = *reinterpret_cast<BwdSmem*>(smraw);
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -289,7 +290,7 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
         const int ch = lane + 32 * j, row = ch >> 4, zq = ch & 15;
         const int64_t r = rb + row < m ? rb + row : m - 1;
         const int64_t zi = z0 + 4 * zq < n ? z0 + 4 * zq : 0;
-        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + r * n + zi);
+        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + r * ldz + zi);
       }
       const int64_t c0 = rb * C / 4;  // 16-byte chunk index of the stage's first delta
       for (int j = lane; j < kBrowStage * C / 4; j += 32)
@@ -393,7 +394,7 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, const float* _
   if (warp == 0) umma::tmem_free<kBwdTmemCols>(tm);
 }
 
-int fused_fwd_tc(const float* z, int64_t m, int64_t n, const float* w, int64_t F, int C,
+int fused_fwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float* w, int64_t F, int C,
                  int64_t col_cos, int64_t col_sin, float* lpart, cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
   const size_t smem = sizeof(FwdSmem);
@@ -411,11 +412,11 @@ int fused_fwd_tc(const float* z, int64_t m, int64_t n, const float* w, int64_t F
   if (rtg > kFwdMaxRTG) rtg = kFwdMaxRTG;
   if (rtg < 1) rtg = 1;
   dim3 grid((unsigned)((RT + rtg - 1) / rtg), (unsigned)KS);
-  return launch_pdl(k_fused_fwd_tc, grid, dim3(kFwdThreads), smem, st, "k_fused_fwd_tc", z, m, n, w,
-                    F, C, col_cos, col_sin, (int)rtg, lpart);
+  return launch_pdl(k_fused_fwd_tc, grid, dim3(kFwdThreads), smem, st, "k_fused_fwd_tc", z, m, n, ldz,
+                    w, F, C, col_cos, col_sin, (int)rtg, lpart);
 }
 
-int fused_bwd_tc(const float* z, int64_t m, int64_t n, const float* delta, int C, int64_t F,
+int fused_bwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float* delta, int C, int64_t F,
                  int64_t col_cos, int64_t col_sin, float* dw, float* w, float lr, float l2,
                  cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
@@ -428,7 +429,7 @@ int fused_bwd_tc(const float* z, int64_t m, int64_t n, const float* delta, int C
   }
   const unsigned grid = (unsigned)((n + kBzCta - 1) / kBzCta);
   return launch_pdl(k_fused_bwd_tc, dim3(grid), dim3(kBwdThreads), smem, st, "k_fused_bwd_tc", z, m, n,
-                    delta, C, F, col_cos, col_sin, dw, w, lr, l2);
+                    ldz, delta, C, F, col_cos, col_sin, dw, w, lr, l2);
 }
 
 int64_t fused_tc_ksplits(int64_t n) { return (n + kFzCta - 1) / kFzCta; }
