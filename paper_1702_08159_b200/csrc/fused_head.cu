@@ -2,15 +2,15 @@
 // (BASELINE config 4: d = n = 16384, E = 32, 2^20 features per row, 10
 // classes).  Features are never written to HBM:
 //
-//   for each pair of blocks: k_fastfood (z of the two blocks only,
-//                         fastfood_z_blocks) -> z tile (m x 2n fp32, scratch)
+//   for each group of 4 blocks: k_fastfood (z of those blocks only,
+//                         fastfood_z_blocks) -> z tile (m x 4n fp32, scratch)
 //     for each block e:   k_fused_fwd_tc: cos/sin computed on chip from z,
 //                         contracted with the W slice of block e on the
 //                         tensor cores into per-chunk partial logits
 //                         k_fused_fold: partial logits -> float64 logits
 //                         (fixed order: blocks ascending, chunks in order)
 //   softmax / loss / delta (classifier.cu, k_head_softmax)
-//   for each pair of blocks: k_fastfood again (recompute z; cheaper than
+//   for each group of 4 blocks: k_fastfood again (recompute z; cheaper than
 //                         storing 2^20 features per row)
 //     for each block e:   k_fused_bwd_tc: dW slice of block e = delta^T
 //                         [cos z | sin z] with cos/sin on chip, written or
@@ -37,10 +37,10 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
 
 constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
 // Blocks whose z the producer computes per launch: (row, block) items fill
-// the producer's waves better (1,024 rows x 2 blocks over 296 CTA slots: 6.9
-// of 7 waves instead of 3.5 of 4) and halve its launches; the tile
+// the producer's waves better (1,024 rows x 4 blocks over 296 CTA slots:
+// 13.8 of 14 waves instead of 3.5 of 4) and cut its launches 4x; the tile
 // (m x kFusedZBlocks*n) is read back by the contractions from L2/HBM.
-constexpr int kFusedZBlocks = 2;
+constexpr int kFusedZBlocks = 4;
 int64_t fused_tc_ksplits(int64_t n);  // fused_tc.cu
 constexpr int kFwarps = 8;
 constexpr int kFrowsPerWarp = 4;
