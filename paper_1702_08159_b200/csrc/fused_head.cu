@@ -4,15 +4,15 @@
 //
 //   for each group of 4 blocks: k_fastfood (z of those blocks only,
 //                         fastfood_z_blocks) -> z tile (m x 4n fp32, scratch)
-//     for each block e:   k_fused_fwd_tc: cos/sin computed on chip from z,
-//                         contracted with the W slice of block e on the
+//                       k_fused_fwd_tc: cos/sin computed on chip from z,
+//                         contracted with the group's W columns on the
 //                         tensor cores into per-chunk partial logits
-//                         k_fused_fold: partial logits -> float64 logits
-//                         (fixed order: blocks ascending, chunks in order)
+//                       k_fused_fold: partial logits -> float64 logits
+//                         (fixed order: groups ascending, chunks in order)
 //   softmax / loss / delta (classifier.cu, k_head_softmax)
 //   for each group of 4 blocks: k_fastfood again (recompute z; cheaper than
 //                         storing 2^20 features per row)
-//     for each block e:   k_fused_bwd_tc: dW slice of block e = delta^T
+//                       k_fused_bwd_tc: dW columns of the group = delta^T
 //                         [cos z | sin z] with cos/sin on chip, written or
 //                         applied as the SGD update in place.
 // (k_fused_fwd / k_fused_bwd / k_fused_dw_finish: the CUDA-core cross-check
@@ -53,13 +53,13 @@ constexpr int kFusedMaxClasses = 16;
 
 struct FusedScratch {
   float* z;          // [m][kFusedZBlocks * n]
-  float* lpart;      // [KS][m][C]     partial logits of the current block
+  float* lpart;      // [KS][m][C]     partial logits of the current block group
   double* logits;    // [m][C]
   double* rowloss;   // [m]
   int32_t* rowhit;   // [m]
   double* delta64;   // [m][C]
   float* delta32;    // [m][C]
-  float* dwpart;     // [RS][C][2n]    backward partials of the current block
+  float* dwpart;     // [RS][C][2 nz]  backward partials of the current block group
 };
 
 inline int64_t fused_rsplits(int64_t m) {
@@ -75,7 +75,8 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
     off += al(bytes);
     return p;
   };
-  const int64_t KS_cc = (n + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(n);
+  const int64_t nz = n * kFusedZBlocks;  // z columns handled per launch group
+  const int64_t KS_cc = (nz + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(nz);
   const int64_t KS = KS_cc > KS_tc ? KS_cc : KS_tc;   // partial-logit chunks of either variant
   FusedScratch s{};
   s.z = (float*)take(m * n * kFusedZBlocks * 4);
@@ -85,7 +86,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
   s.rowhit = (int32_t*)take(m * 4);
   s.delta64 = (double*)take(m * C * 8);
   s.delta32 = (float*)take(m * C * 4);
-  s.dwpart = (float*)take(fused_rsplits(m) * C * 2 * n * 4);
+  s.dwpart = (float*)take(fused_rsplits(m) * C * 2 * nz * 4);
   if (fs) *fs = s;
   return off;
 }
@@ -305,20 +306,21 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;
   fused_layout(m, n, C, (char*)scratch, &fs);
-  const int64_t KS = cuda_cores ? (n + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(n);
+  // Blocks e .. e+nb-1 are contiguous in z (tile columns), in W (cos and
+  // sin columns) and in the partial-logit chunks: one contraction and one
+  // fold per group, over nb*n z values.
   const int64_t ldz = n * kFusedZBlocks;
-  for (int32_t e = 0; e < E; ++e) {
-    const int32_t zb = e % kFusedZBlocks;  // block's column slot in the z tile
-    if (zb == 0)
-      MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e,
-                                (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks), fs.z, ldz, st));
-    const float* zt = fs.z + (int64_t)zb * n;
+  for (int32_t e = 0; e < E; e += kFusedZBlocks) {
+    const int32_t nb = (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks);
+    const int64_t nz = (int64_t)nb * n;
+    const int64_t KS = cuda_cores ? (nz + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(nz);
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, fs.z, ldz, st));
     if (!cuda_cores)
-      MCK_TRY(fused_fwd_tc(zt, m, n, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+      MCK_TRY(fused_fwd_tc(fs.z, m, nz, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
     else MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
-      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(zt, m, n, ldz, w, F, (int64_t)e * n,
+      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(fs.z, m, nz, ldz, w, F, (int64_t)e * n,
                                                      D + (int64_t)e * n, fs.lpart);
       return check_launch("k_fused_fwd");
     }));
@@ -346,26 +348,24 @@ int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x
   k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
   MCK_TRY(check_launch("k_to_f32"));
   const int64_t ldz = n * kFusedZBlocks;
-  for (int32_t e = 0; e < E; ++e) {
-    const int32_t zb = e % kFusedZBlocks;
-    if (zb == 0)
-      MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e,
-                                (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks), fs.z, ldz, st));
-    const float* zt = fs.z + (int64_t)zb * n;
+  for (int32_t e = 0; e < E; e += kFusedZBlocks) {
+    const int32_t nb = (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks);
+    const int64_t nz = (int64_t)nb * n;
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, fs.z, ldz, st));
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_tc(zt, m, n, ldz, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw, w,
-                           (float)lr, (float)l2, st));
+      MCK_TRY(fused_bwd_tc(fs.z, m, nz, ldz, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw,
+                           w, (float)lr, (float)l2, st));
       continue;
     }
     MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
-      dim3 grid((unsigned)((n + kBz - 1) / kBz), (unsigned)RS);
-      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(zt, m, n, ldz, fs.delta32, rps, fs.dwpart);
+      dim3 grid((unsigned)((nz + kBz - 1) / kBz), (unsigned)RS);
+      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(fs.z, m, nz, ldz, fs.delta32, rps, fs.dwpart);
       return check_launch("k_fused_bwd");
     }));
-    int64_t grid = ((int64_t)C * 2 * n + 255) / 256;
+    int64_t grid = ((int64_t)C * 2 * nz + 255) / 256;
     if (grid > 148 * 8) grid = 148 * 8;
-    k_fused_dw_finish<<<(unsigned)grid, 256, 0, st>>>(fs.dwpart, RS, C, n, F, (int64_t)e * n,
+    k_fused_dw_finish<<<(unsigned)grid, 256, 0, st>>>(fs.dwpart, RS, C, nz, F, (int64_t)e * n,
                                                       D + (int64_t)e * n, dw, w, (float)lr,
                                                       (float)l2);
     MCK_TRY(check_launch("k_fused_dw_finish"));
