@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(kFwarps * 32) k_fused_fwd(const float* __restr
 }
 
 // logits[r][c] (+)= sum_ks lpart[ks][r][c]   (float64, chunk order)
-// 32 outputs per CTA; warp w sums the partials k = w, w+8, ... and the eight
+// 32 outputs per CTA; warp w sums the partials k = w, w+32, ... and the 32
 // warp sums are combined in a fixed order (deterministic, independent loads).
-constexpr int kFoldWarps = 8;
+constexpr int kFoldWarps = 32;
 __global__ void __launch_bounds__(kFoldWarps * 32)
 k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C, double* logits,
              int first) {
