@@ -1,22 +1,25 @@
 // K3 -- fused Fastfood expansion (replaces fastfood.py:179-226:
 // apply_zhat_batch + feature_map_batch).
 //
-// One thread group (T threads, R = n/T values each) owns one input row.  The
-// row is read once from HBM (16-byte loads, zero padding implicit) and kept
-// in registers for all E blocks.  Per block:
+// Per row and block e:
 //   x*B  : sign-bit XOR from a per-thread mask word          (fastfood.py:190)
 //   H    : register butterflies + shared-memory exchanges     (:191)
-//   Pi,G : one scatter into shared memory: z1[j] goes to perm^-1[j]'s slot
-//          already multiplied by g[perm^-1[j]] (the same fp32 product the
-//          reference forms after its gather, :192-193); slots are edge-
-//          coloured so scatter and gather are bank-conflict free
+//   Pi,G : one scatter into shared memory and one gather; slots are edge-
+//          coloured so scatter and gather are bank-conflict free, and the
+//          product z1[perm[p]] * g[p] is the same fp32 product the reference
+//          forms after its gather (:192-193)
 //   H    : middle rounds first, ending in the 16-byte store layout (:194)
 //   C*s  : one multiply when 1/(sigma*sqrt n) is a power of two (exactly the
 //          reference's two roundings), else two               (:195-196)
-//   cos/sin epilogue with 2*pi range reduction, [cos | sin] halves, optional
-//          float32(1/sqrt(D)) (:220-225); 16-byte stores.
+//   cos/sin epilogue (MUFU), [cos | sin] halves, optional float32(1/sqrt(D))
+//          (:220-225); 16-byte stores.
 // HBM traffic is one read of x and one write of the features.
 //
+// k_fastfood_pair (n = 1024, c0/c2/c3): two rows per warp, packed f32x2,
+//   block-major work units, TMA-staged tables and x rows.
+// k_fastfood (other n): one row per thread group; x kept in registers for all
+//   E blocks for n <= 8192; n = 16384 (c4) runs 512-thread rows over
+//   balanced (row, block) item ranges and reads its tables through L1/L2.
 // The `parity` variant restates the reference arithmetic exactly (sequential
 // base-256 sums, (a+b)-2b combine, separate roundings) for bit-exact z checks.
 #include "mck_common.cuh"
@@ -366,10 +369,11 @@ __device__ __forceinline__ void st_out(float4* p, float4 v) { *p = v; }
 // row1[i]) of one index i, so every butterfly stage is a packed f32x2 add/sub
 // (including the stage on the lowest register bit that the one-row kernel
 // leaves scalar), every exchange moves both rows with one 8-byte access, and
-// each table entry (scatter offset + g, gather colour, C*scale, sign mask) is
-// loaded once for two rows.  x is re-read per block (L1-resident) instead of
-// being held in registers.  Exchanges use the 8-byte padding pad2 (conflict
-// free per 16-lane phase for layouts L and P0); Pi uses 16-colour slots.
+// each table entry (16-bit scatter offset, g in the gather layout, gather
+// colour, C*scale, sign mask) is loaded once for two rows.  x is re-read per
+// block (TMA-staged, L2-resident) instead of being held in registers.
+// Exchanges use the 8-byte padding pad2 (conflict free per 16-lane phase for
+// layouts L and P0); Pi uses 16-colour slots.
 __host__ __device__ constexpr uint32_t pad2(uint32_t i) { return i + (i >> 4) + 4 * (i >> 7); }
 constexpr int kPairRowFloat2 = 1116;  // pad2(1023) + 1, rounded to 16 bytes
 constexpr int kPairWarps = 8;
