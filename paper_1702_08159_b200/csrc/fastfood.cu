@@ -285,29 +285,52 @@ k_fastfood(FFParams p) {
       // ---- H (first)
       butterflies<R, C::PL, C::PL>(v);
       middle_rounds<C, 0, C::PL>(s, tid, gid, v);
-      // ---- Pi and G: scatter z1[j] * g[perm^-1[j]] to perm^-1[j]
-      // table loads batched ahead of the stores: the compiler cannot hoist a
-      // shared load above a shared store to an unknown address by itself
+      // ---- Pi and G.  Tables read through L1/L2 (n = 16384): 16-bit slot
+      // offsets (eight per 16-byte load), then G from a gather-layout table
+      // after the gather (y[p] = z1[perm[p]] * g[p]).  Staged tables: one
+      // scatter of z1[j] * g[perm^-1[j]] (the same fp32 product), table loads
+      // batched ahead of the stores (the compiler cannot hoist a shared load
+      // above a shared store to an unknown address by itself).
+      constexpr bool COMPACT = !STAGED && ff_colored<C>();
+      if constexpr (COMPACT) {
+        const uint4* t_so = reinterpret_cast<const uint4*>(p.soff + (int64_t)(p.e0 + e) * N);
 #pragma unroll
-      for (int k0 = 0; k0 < R; k0 += 8) {
-        uint2 a[8];
+        for (int k0 = 0; k0 < R; k0 += 8) {
+          const uint4 o = __ldg(t_so + (k0 / 8) * T + tid);
+          const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-        for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + tid];
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float*>(reinterpret_cast<char*>(s) + ((ow[q / 2] >> (16 * (q % 2))) & 0xffffu)) =
+                v[k0 + q];
+        }
+      } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float*>(reinterpret_cast<char*>(s) + a[q].x) =
-              v[k0 + q] * __uint_as_float(a[q].y);
+        for (int k0 = 0; k0 < R; k0 += 8) {
+          uint2 a[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) a[q] = t_scat[(k0 + q) * T + tid];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float*>(reinterpret_cast<char*>(s) + a[q].x) =
+                v[k0 + q] * __uint_as_float(a[q].y);
+        }
       }
       group_sync<T>(gid);
       if constexpr (ff_colored<C>()) {
         // gather group (warp w, register k) occupies words 32*(w*R + k) + colour
         const char* gb = reinterpret_cast<const char*>(s) + (tid / 32) * (R * 128);
+        const float4* t_g4 = reinterpret_cast<const float4*>(p.ggath + (int64_t)(p.e0 + e) * N);
 #pragma unroll
         for (int k4 = 0; k4 < R / 4; ++k4) {
           const uint32_t cw = t_gc[k4 * T + tid];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             v[4 * k4 + q] = *reinterpret_cast<const float*>(gb + (4 * k4 + q) * 128 + ((cw >> (8 * q)) & 0xffu));
+          if constexpr (COMPACT) {
+            const float4 g4 = __ldg(t_g4 + k4 * T + tid);
+            mul_pk(v[4 * k4], v[4 * k4 + 1], g4.x, g4.y);
+            mul_pk(v[4 * k4 + 2], v[4 * k4 + 3], g4.z, g4.w);
+          }
         }
       } else {
         lds_layout<R, P0>(s, thread_part<C::FULL, P0>(tid), v);
@@ -770,8 +793,9 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
     }
   std::vector<uint2> scat((size_t)E * N);
   std::vector<uint32_t> gcol((size_t)E * N / 4, 0u);
-  std::vector<uint16_t> soff(PAIR ? (size_t)E * N : 0);
-  std::vector<float> ggath(PAIR ? (size_t)E * N : 0);
+  static_assert(R % 8 == 0, "coloured layouts hold 32 registers");
+  std::vector<uint16_t> soff((size_t)E * N);
+  std::vector<float> ggath((size_t)E * N);
   std::vector<int32_t> left(N), right(N);
   std::vector<uint8_t> col(N);
   for (int e = 0; e < E; ++e) {
@@ -788,7 +812,7 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
           make_uint2((uint32_t)ES * ((uint32_t)GW * (uint32_t)ggrp[p] + col[j]), gbits[(size_t)e * N + p]);
       const int k = gpos[p] / T, t = gpos[p] % T;
       gcol[(size_t)e * (N / 4) + (k / 4) * T + t] |= ((uint32_t)ES * col[j]) << (8 * (k % 4));
-      if constexpr (PAIR) {
+      {
         const uint32_t off = (uint32_t)ES * ((uint32_t)GW * (uint32_t)ggrp[p] + col[j]);
         if (off > 0xffffu) return fail_value("internal: scatter offset exceeds 16 bits");
         const int sk = spos[j] / T, st_ = spos[j] % T;
@@ -800,12 +824,10 @@ int color_tables(const TablesView& tv, cudaStream_t st) {
       }
     }
   }
-  if constexpr (PAIR) {
-    MCK_TRY(check_cuda(cudaMemcpyAsync(tv.soff, soff.data(), soff.size() * 2,
-                                       cudaMemcpyHostToDevice, st), "soff H2D"));
-    MCK_TRY(check_cuda(cudaMemcpyAsync(tv.ggath, ggath.data(), ggath.size() * 4,
-                                       cudaMemcpyHostToDevice, st), "ggath H2D"));
-  }
+  MCK_TRY(check_cuda(cudaMemcpyAsync(tv.soff, soff.data(), soff.size() * 2,
+                                     cudaMemcpyHostToDevice, st), "soff H2D"));
+  MCK_TRY(check_cuda(cudaMemcpyAsync(tv.ggath, ggath.data(), ggath.size() * 4,
+                                     cudaMemcpyHostToDevice, st), "ggath H2D"));
   MCK_TRY(check_cuda(cudaMemcpyAsync(tv.scat, scat.data(), scat.size() * 8,
                                      cudaMemcpyHostToDevice, st), "scat H2D"));
   MCK_TRY(check_cuda(cudaMemcpyAsync(tv.gcol, gcol.data(), gcol.size() * 4,
