@@ -13,6 +13,7 @@
 #include <type_traits>
 
 #include "mck_common.cuh"
+#include "async_copy.cuh"
 
 namespace mck {
 
@@ -64,14 +65,30 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_head_fwd(const float* __rest
                                                              const double* __restrict__ w,
                                                              double* __restrict__ partial) {
   extern __shared__ __align__(16) double ws[];  // [NC][kFwdK]
+  __shared__ uint64_t wbar;
   const int ks = blockIdx.y;
   const int64_t f0 = (int64_t)ks * kFwdK;
   const int nf = (int)((F - f0) < kFwdK ? (F - f0) : kFwdK);
-  for (int t = threadIdx.x; t < NC * kFwdK; t += blockDim.x) {
-    const int c = t / kFwdK, f = t % kFwdK;
-    ws[t] = f < nf ? w[(int64_t)c * F + f0 + f] : 0.0;
+  // W slice: one TMA bulk copy per class row (contiguous in W) when the rows
+  // are 16-byte aligned, else a plain loop; columns past F are zeroed.
+  const bool bulk = (F % 2 == 0) && ((reinterpret_cast<uintptr_t>(w) & 15) == 0);
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      mbar_init(&wbar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&wbar, (uint32_t)(NC * nf * 8));
+      for (int c = 0; c < NC; ++c) bulk_g2s(ws + c * kFwdK, w + (int64_t)c * F + f0, (uint32_t)nf * 8, &wbar);
+    }
+    for (int t = threadIdx.x; t < NC * kFwdK; t += blockDim.x)
+      if (t % kFwdK >= nf) ws[t] = 0.0;
+  } else {
+    for (int t = threadIdx.x; t < NC * kFwdK; t += blockDim.x) {
+      const int c = t / kFwdK, f = t % kFwdK;
+      ws[t] = f < nf ? w[(int64_t)c * F + f0 + f] : 0.0;
+    }
   }
   __syncthreads();
+  if (bulk) mbar_wait(&wbar, 0u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)blockIdx.x * kFwdRows + warp * kFwdRowsPerWarp;
   double acc[kFwdRowsPerWarp][NC];
