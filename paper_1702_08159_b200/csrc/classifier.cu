@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_head_bwd(const float* __restric
     for (int t = threadIdx.x; t < nr * NC; t += blockDim.x) sd[t / NC][t % NC] = delta[r0 * NC + t];
     __syncthreads();
     const float* pp = phi + r0 * ld;
-#pragma unroll 2
+#pragma unroll 4
     for (int rr = 0; rr < nr; ++rr) {
       double x[kBwdFeatPerThread];
 #pragma unroll
