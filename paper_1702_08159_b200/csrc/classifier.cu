@@ -135,38 +135,48 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_head_fwd(const float* __rest
   }
 }
 
-// logits -> stable softmax (linear_model.py:79-83) -> loss / delta / argmax
-__global__ void k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
-                               const double* __restrict__ b, const int32_t* __restrict__ labels,
-                               const int32_t* __restrict__ label_index, int64_t m_total,
-                               double* probs, double* delta, double* rowloss, int32_t* rowhit) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= m) return;
-  double z[kMaxClasses];
-  for (int c = 0; c < C; ++c) {
-    double s = 0.0;
-    for (int64_t k = 0; k < KS; ++k) s += partial[(k * m + r) * C + c];
-    z[c] = s + b[c];
+// logits -> stable softmax (linear_model.py:79-83) -> loss / delta / argmax.
+// One CTA per kSmRows rows: thread (row, class) sums the split-K partials of
+// its logit in ascending split order (loads of all splits in flight), then one
+// thread per row finishes the softmax from shared memory.
+constexpr int kSmRows = 32;
+__global__ void __launch_bounds__(kSmRows * kMaxClasses)
+k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
+               const double* __restrict__ b, const int32_t* __restrict__ labels,
+               const int32_t* __restrict__ label_index, int64_t m_total, double* probs,
+               double* delta, double* rowloss, int32_t* rowhit) {
+  __shared__ double zs[kSmRows][kMaxClasses];
+  const int rr = threadIdx.x / kMaxClasses, c = threadIdx.x % kMaxClasses;
+  const int64_t r = (int64_t)blockIdx.x * kSmRows + rr;
+  if (r < m && c < C) {
+    double sum = 0.0;
+#pragma unroll 8
+    for (int64_t k = 0; k < KS; ++k) sum += partial[(k * m + r) * C + c];
+    zs[rr][c] = sum + b[c];
   }
+  __syncthreads();
+  if (c != 0 || r >= m) return;
+  double* z = zs[rr];
   double mx = z[0];
-  for (int c = 1; c < C; ++c) mx = fmax(mx, z[c]);
-  for (int c = 0; c < C; ++c) z[c] = exp(z[c] - mx);
+  for (int j = 1; j < C; ++j) mx = fmax(mx, z[j]);
+  for (int j = 0; j < C; ++j) z[j] = exp(z[j] - mx);
   const double sum = pairwise_serial([&](int64_t i) { return z[i]; }, 0, C);
   int arg = 0;
-  for (int c = 0; c < C; ++c) {
-    z[c] /= sum;
-    if (z[c] > z[arg]) arg = c;  // first maximum, as numpy argmax
+  for (int j = 0; j < C; ++j) {
+    z[j] /= sum;
+    if (z[j] > z[arg]) arg = j;  // first maximum, as numpy argmax
   }
   const int y = labels ? labels[label_index ? label_index[r] : r] : -1;
   if (probs)
-    for (int c = 0; c < C; ++c) probs[r * C + c] = z[c];
+    for (int j = 0; j < C; ++j) probs[r * C + j] = z[j];
   if (y >= 0) {
     rowloss[r] = -log(fmax(z[y], 1e-300));
     rowhit[r] = (arg == y) ? 1 : 0;
     if (delta)
-      for (int c = 0; c < C; ++c) delta[r * C + c] = (z[c] - (c == y ? 1.0 : 0.0)) / (double)m_total;
+      for (int j = 0; j < C; ++j) delta[r * C + j] = (z[j] - (j == y ? 1.0 : 0.0)) / (double)m_total;
   }
 }
+
 
 // fixed-order reduction of per-row loss / hits (one CTA)
 __global__ void k_head_reduce(const double* rowloss, const int32_t* rowhit, int64_t m,
@@ -228,7 +238,7 @@ int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const doubl
     default: return fail_value("num_classes must be in 2..%d", kMaxClasses);
   }
   MCK_TRY(rc);
-  k_head_softmax<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+  k_head_softmax<<<(unsigned)((m + kSmRows - 1) / kSmRows), kSmRows * kMaxClasses, 0, st>>>(
       hs.partial, head_ksplits(F), m, C, b, labels, label_index, m_total, probs, delta,
       hs.rowloss, hs.rowhit);
   MCK_TRY(check_launch("k_head_softmax"));
@@ -399,7 +409,7 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
                              double* rowloss, int32_t* rowhit, cudaStream_t st) {
   if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
   if (m == 0) return MCK_OK;
-  k_head_softmax<<<(unsigned)((m + 127) / 128), 128, 0, st>>>(
+  k_head_softmax<<<(unsigned)((m + kSmRows - 1) / kSmRows), kSmRows * kMaxClasses, 0, st>>>(
       logits, 1, m, C, b, labels, label_index, m_total, probs, delta, rowloss, rowhit);
   MCK_TRY(check_launch("k_head_softmax"));
   if (labels && (loss_sum || hits)) {
