@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_head_fwd(const float* __rest
                                                              int64_t m, int64_t F, int64_t ld,
                                                              const double* __restrict__ w,
                                                              double* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) double ws[];  // [NC][kFwdK]
   __shared__ uint64_t wbar;
   const int ks = blockIdx.y;
@@ -145,6 +147,8 @@ k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
                const double* __restrict__ b, const int32_t* __restrict__ labels,
                const int32_t* __restrict__ label_index, int64_t m_total, double* probs,
                double* delta, double* rowloss, int32_t* rowhit) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double zs[kSmRows][kMaxClasses];
   const int rr = threadIdx.x / kMaxClasses, c = threadIdx.x % kMaxClasses;
   const int64_t r = (int64_t)blockIdx.x * kSmRows + rr;
@@ -181,6 +185,8 @@ k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
 // fixed-order reduction of per-row loss / hits (one CTA)
 __global__ void k_head_reduce(const double* rowloss, const int32_t* rowhit, int64_t m,
                               double* loss_sum, int64_t* hits) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sl[1024];
   __shared__ long long sh[1024];
   double a = 0.0;
@@ -214,8 +220,7 @@ int launch_fwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double*
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "head fwd smem"));
   dim3 grid((unsigned)((m + kFwdRows - 1) / kFwdRows), (unsigned)head_ksplits(F));
-  kern<<<grid, kFwdWarps * 32, smem, st>>>(phi, m, F, ld, w, partial);
-  return check_launch("k_head_fwd");
+  return launch_pdl(kern, grid, dim3(kFwdWarps * 32), smem, st, "k_head_fwd", phi, m, F, ld, w, partial);
 }
 
 int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
@@ -238,13 +243,13 @@ int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const doubl
     default: return fail_value("num_classes must be in 2..%d", kMaxClasses);
   }
   MCK_TRY(rc);
-  k_head_softmax<<<(unsigned)((m + kSmRows - 1) / kSmRows), kSmRows * kMaxClasses, 0, st>>>(
-      hs.partial, head_ksplits(F), m, C, b, labels, label_index, m_total, probs, delta,
-      hs.rowloss, hs.rowhit);
-  MCK_TRY(check_launch("k_head_softmax"));
+  MCK_TRY(launch_pdl(k_head_softmax, dim3((unsigned)((m + kSmRows - 1) / kSmRows)),
+                     dim3(kSmRows * kMaxClasses), 0, st, "k_head_softmax", (const double*)hs.partial,
+                     head_ksplits(F), m, (int)C, b, labels, label_index, m_total, probs, delta,
+                     hs.rowloss, hs.rowhit));
   if (labels && (loss_sum || hits)) {
-    k_head_reduce<<<1, 1024, 0, st>>>(hs.rowloss, hs.rowhit, m, loss_sum, hits);
-    MCK_TRY(check_launch("k_head_reduce"));
+    MCK_TRY(launch_pdl(k_head_reduce, dim3(1), dim3(1024), 0, st, "k_head_reduce",
+                       (const double*)hs.rowloss, (const int32_t*)hs.rowhit, m, loss_sum, hits));
   }
   return MCK_OK;
 }
@@ -256,6 +261,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_head_bwd(const float* __restric
                                                           const double* __restrict__ delta,
                                                           int64_t rows_per_split,
                                                           double* __restrict__ dwpart) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double sd[kBwdRowChunk][NC];
   const int rs = blockIdx.y;
   const int64_t rbeg = (int64_t)rs * rows_per_split;
@@ -300,6 +307,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_head_bwd(const float* __restric
 // dW = sum over row splits (fixed order); optionally W -= lr*(dW + 2*l2*W)
 __global__ void k_head_dw_finish(const double* __restrict__ dwpart, int64_t RS, int64_t total,
                                  double* dw, double* w, double lr, double l2) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     double g = 0.0;
@@ -316,6 +325,8 @@ __global__ void k_head_dw_finish(const double* __restrict__ dwpart, int64_t RS, 
 
 // db[c] = sum_r delta[r][c] in a fixed order; optionally b -= lr*db.  One CTA per class.
 __global__ void k_head_db(const double* delta, int64_t m, int C, double* db, double* b, double lr) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double s[256];
   const int c = blockIdx.x;
   double a = 0.0;
@@ -337,7 +348,8 @@ int launch_bwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double*
                const HeadScratch& hs, int64_t RS, cudaStream_t st) {
   const int64_t rows_per_split = (m + RS - 1) / RS;
   dim3 grid((unsigned)((F + kBwdK - 1) / kBwdK), (unsigned)RS);
-  k_head_bwd<NC><<<grid, kBwdThreads, 0, st>>>(phi, m, F, ld, delta, rows_per_split, hs.dwpart);
+  MCK_TRY(launch_pdl(k_head_bwd<NC>, grid, dim3(kBwdThreads), 0, st, "k_head_bwd", phi, m, F, ld, delta,
+                     rows_per_split, hs.dwpart));
   return check_launch("k_head_bwd");
 }
 
@@ -364,10 +376,9 @@ static int head_bwd_common(const float* phi, int64_t m, int64_t F, int64_t ld,
   const int64_t total = (int64_t)C * F;
   int64_t grid = (total + 255) / 256;
   if (grid > 148 * 8) grid = 148 * 8;
-  k_head_dw_finish<<<(unsigned)grid, 256, 0, st>>>(hs.dwpart, RS, total, dw, w, lr, l2);
-  MCK_TRY(check_launch("k_head_dw_finish"));
-  k_head_db<<<C, 256, 0, st>>>(delta, m, C, db, b, lr);
-  return check_launch("k_head_db");
+  MCK_TRY(launch_pdl(k_head_dw_finish, dim3((unsigned)grid), dim3(256), 0, st, "k_head_dw_finish",
+                     (const double*)hs.dwpart, RS, total, dw, w, lr, l2));
+  return launch_pdl(k_head_db, dim3(C), dim3(256), 0, st, "k_head_db", delta, m, (int)C, db, b, lr);
 }
 
 int head_backward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
@@ -409,12 +420,12 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
                              double* rowloss, int32_t* rowhit, cudaStream_t st) {
   if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
   if (m == 0) return MCK_OK;
-  k_head_softmax<<<(unsigned)((m + kSmRows - 1) / kSmRows), kSmRows * kMaxClasses, 0, st>>>(
-      logits, 1, m, C, b, labels, label_index, m_total, probs, delta, rowloss, rowhit);
-  MCK_TRY(check_launch("k_head_softmax"));
+  MCK_TRY(launch_pdl(k_head_softmax, dim3((unsigned)((m + kSmRows - 1) / kSmRows)),
+                     dim3(kSmRows * kMaxClasses), 0, st, "k_head_softmax", logits, (int64_t)1, m, (int)C,
+                     b, labels, label_index, m_total, probs, delta, rowloss, rowhit));
   if (labels && (loss_sum || hits)) {
-    k_head_reduce<<<1, 1024, 0, st>>>(rowloss, rowhit, m, loss_sum, hits);
-    MCK_TRY(check_launch("k_head_reduce"));
+    MCK_TRY(launch_pdl(k_head_reduce, dim3(1), dim3(1024), 0, st, "k_head_reduce",
+                       (const double*)rowloss, (const int32_t*)rowhit, m, loss_sum, hits));
   }
   return MCK_OK;
 }
