@@ -35,6 +35,7 @@ struct HeadScratch {
 };
 
 inline int64_t head_ksplits(int64_t F) { return (F + kFwdK - 1) / kFwdK; }
+inline int64_t head_ksplits_max(int64_t F) { return (F + 511) / 512; }  // k_head_fwd_dmma (kDK)
 inline int64_t head_rsplits(int64_t m, int64_t F, int32_t C) {
   int64_t rs = (int64_t(1) << 22) / ((int64_t)C * F);  // keep dW partials <= 32 MB
   if (rs > 16) rs = 16;
@@ -47,7 +48,7 @@ inline int64_t head_layout(int64_t m, int64_t F, int32_t C, char* base, HeadScra
   int64_t off = 0;
   HeadScratch h{};
   h.partial = (double*)(base ? base + off : nullptr);
-  off += al(head_ksplits(F) * m * C * 8);
+  off += al(head_ksplits_max(F) * m * C * 8);
   h.rowloss = (double*)(base ? base + off : nullptr);
   off += al(m * 8);
   h.rowhit = (int32_t*)(base ? base + off : nullptr);
@@ -137,6 +138,70 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_head_fwd(const float* __rest
   }
 }
 
+// Same contraction on the FP64 tensor cores (mma.sync.m8n8k4.f64): a warp
+// owns 8 rows, a CTA 64 rows x 512 features; classes are padded to N tiles of
+// 8.  Per 16-feature group each lane loads one float4 of its row (the K order
+// inside the group is permuted so that lane k of the fragment owns features
+// 16u + 4k .. 16u + 4k + 3), and per k-step one W value per N tile from shared
+// memory (row stride 513 doubles: conflict-free fragments).  float64 products
+// and sums as before, in a different (fixed) order.
+constexpr int kDK = 512;  // (head_ksplits_max sizes the partials for it)
+constexpr int kDRows = 64;
+constexpr int kDStride = kDK + 1;
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_head_fwd_dmma(const float* __restrict__ phi, int64_t m,
+                                                       int64_t F, int64_t ld,
+                                                       const double* __restrict__ w,
+                                                       double* __restrict__ partial) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NT = (NC + 7) / 8;
+  extern __shared__ __align__(16) double wsd[];  // [NT*8][kDStride]
+  const int ks = blockIdx.y;
+  const int64_t f0 = (int64_t)ks * kDK;
+  const int nf = (int)((F - f0) < kDK ? (F - f0) : kDK);  // multiple of 16 (host check)
+#pragma unroll 4
+  for (int t = threadIdx.x; t < NT * 8 * kDK; t += blockDim.x) {
+    const int c = t / kDK, f = t % kDK;
+    wsd[c * kDStride + f] = (c < NC && f < nf) ? w[(int64_t)c * F + f0 + f] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kc = lane & 3, n = lane >> 2;
+  const int64_t r0 = (int64_t)blockIdx.x * kDRows + warp * 8;
+  const int64_t row = r0 + n < m ? r0 + n : m - 1;  // clamp: duplicates are discarded
+  const float* pr = phi + row * ld + f0 + 4 * kc;
+  const double* wb = wsd + n * kDStride + 4 * kc;
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll 2
+  for (int u = 0; u < nf / 16; ++u) {
+    const float4 a4 = __ldg(reinterpret_cast<const float4*>(pr + 16 * u));
+    const double a[4] = {(double)a4.x, (double)a4.y, (double)a4.z, (double)a4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) dmma_m8n8k4(acc[t], a[j], wb[t * 8 * kDStride + 16 * u + j]);
+  }
+  const int64_t r = r0 + n;
+  if (r < m)
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = 8 * t + 2 * kc + i;
+        if (c < NC) partial[((int64_t)ks * m + r) * NC + c] = acc[t][i];
+      }
+}
+
 // logits -> stable softmax (linear_model.py:79-83) -> loss / delta / argmax.
 // One CTA per kSmRows rows: thread (row, class) sums the split-K partials of
 // its logit in ascending split order (loads of all splits in flight), then one
@@ -213,13 +278,30 @@ __global__ void k_head_reduce(const double* rowloss, const int32_t* rowhit, int6
 
 template <int NC>
 int launch_fwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
-               double* partial, cudaStream_t st) {
+               double* partial, cudaStream_t st, int64_t* ksplits) {
+  // tensor-core path when rows load as float4 and 16-feature groups tile F
+  const bool dmma = (F % 16 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0);
+  if (dmma) {
+    constexpr int NT = (NC + 7) / 8;
+    const size_t smem = (size_t)NT * 8 * kDStride * sizeof(double);
+    auto kern = k_head_fwd_dmma<NC>;
+    static bool init = false;
+    if (!init) {
+      MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem), "head fwd dmma smem"));
+      init = true;
+    }
+    *ksplits = (F + kDK - 1) / kDK;
+    dim3 grid((unsigned)((m + kDRows - 1) / kDRows), (unsigned)*ksplits);
+    return launch_pdl(kern, grid, dim3(256), smem, st, "k_head_fwd_dmma", phi, m, F, ld, w, partial);
+  }
   const size_t smem = (size_t)NC * kFwdK * sizeof(double);
   auto kern = k_head_fwd<NC>;
   if (smem > 48 * 1024)
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "head fwd smem"));
-  dim3 grid((unsigned)((m + kFwdRows - 1) / kFwdRows), (unsigned)head_ksplits(F));
+  *ksplits = head_ksplits(F);
+  dim3 grid((unsigned)((m + kFwdRows - 1) / kFwdRows), (unsigned)*ksplits);
   return launch_pdl(kern, grid, dim3(kFwdWarps * 32), smem, st, "k_head_fwd", phi, m, F, ld, w, partial);
 }
 
@@ -231,8 +313,9 @@ int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const doubl
   if (m == 0) return MCK_OK;
   HeadScratch hs;
   head_layout(m, F, C, (char*)scratch, &hs);
+  int64_t ksplits = 0;
   auto fwd = [&](auto nc) {
-    return launch_fwd<decltype(nc)::value>(phi, m, F, ld, w, hs.partial, st);
+    return launch_fwd<decltype(nc)::value>(phi, m, F, ld, w, hs.partial, st, &ksplits);
   };
   int rc;
   switch (C) {
@@ -245,7 +328,7 @@ int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const doubl
   MCK_TRY(rc);
   MCK_TRY(launch_pdl(k_head_softmax, dim3((unsigned)((m + kSmRows - 1) / kSmRows)),
                      dim3(kSmRows * kMaxClasses), 0, st, "k_head_softmax", (const double*)hs.partial,
-                     head_ksplits(F), m, (int)C, b, labels, label_index, m_total, probs, delta,
+                     ksplits, m, (int)C, b, labels, label_index, m_total, probs, delta,
                      hs.rowloss, hs.rowhit));
   if (labels && (loss_sum || hits)) {
     MCK_TRY(launch_pdl(k_head_reduce, dim3(1), dim3(1024), 0, st, "k_head_reduce",
