@@ -182,8 +182,24 @@ __global__ void __launch_bounds__(256) k_head_fwd_dmma(const float* __restrict__
   double acc[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-#pragma unroll 2
-  for (int u = 0; u < nf / 16; ++u) {
+  // eight float4 loads in flight per lane (nf / 16 is a multiple of 8 except
+  // for a short last chunk, handled by the remainder loop)
+  const int groups = nf / 16;
+  int u = 0;
+  for (; u + 8 <= groups; u += 8) {
+    float4 a4[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) a4[v] = __ldg(reinterpret_cast<const float4*>(pr + 16 * (u + v)));
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const double a[4] = {(double)a4[v].x, (double)a4[v].y, (double)a4[v].z, (double)a4[v].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma_m8n8k4(acc[t], a[j], wb[t * 8 * kDStride + 16 * (u + v) + j]);
+    }
+  }
+  for (; u < groups; ++u) {
     const float4 a4 = __ldg(reinterpret_cast<const float4*>(pr + 16 * u));
     const double a[4] = {(double)a4.x, (double)a4.y, (double)a4.z, (double)a4.w};
 #pragma unroll
