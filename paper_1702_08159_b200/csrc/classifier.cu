@@ -442,10 +442,80 @@ __global__ void k_head_db(const double* delta, int64_t m, int C, double* db, dou
   }
 }
 
+// dW on the FP64 tensor cores: D (classes x features) = delta^T (classes x
+// rows) * phi (rows x features), mma.sync.m8n8k4.f64 with M = classes (tiles
+// of 8), K = 4 rows per step, N = features.  A warp owns 32 features as four
+// N tiles whose columns are the features base + 4n + j (n = 0..7, tile j), so
+// every lane loads one float4 of a row per k-step; delta comes from a shared
+// tile with row stride 20 doubles (conflict-free A fragments).
+constexpr int kBDF = 256;  // features per CTA (8 warps x 32)
+constexpr int kBDS = 20;   // delta tile row stride (doubles)
+
+template <int NC>
+__global__ void __launch_bounds__(256) k_head_bwd_dmma(const float* __restrict__ phi, int64_t m,
+                                                       int64_t F, int64_t ld,
+                                                       const double* __restrict__ delta,
+                                                       int64_t rows_per_split,
+                                                       double* __restrict__ dwpart) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int MT = (NC + 7) / 8;
+  __shared__ double sd[kBwdRowChunk][kBDS];
+  const int rs = blockIdx.y;
+  const int64_t rbeg = (int64_t)rs * rows_per_split;
+  const int64_t rend = rbeg + rows_per_split < m ? rbeg + rows_per_split : m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kc = lane & 3, n = lane >> 2;
+  const int64_t base = (int64_t)blockIdx.x * kBDF + warp * 32;
+  const int64_t fl = base + 4 * n;  // this lane's float4 of every row
+  double acc[MT][4][2];
+#pragma unroll
+  for (int t = 0; t < MT; ++t)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[t][j][0] = acc[t][j][1] = 0.0;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kBwdRowChunk) {
+    const int nr = (int)(rend - r0 < kBwdRowChunk ? rend - r0 : kBwdRowChunk);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kBwdRowChunk * 16; t += blockDim.x) {
+      const int rr = t >> 4, c = t & 15;
+      sd[rr][c] = (rr < nr && c < NC) ? delta[(r0 + rr) * NC + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k0 = 0; k0 < nr; k0 += 4) {
+      const int64_t row = r0 + k0 + kc < rend ? r0 + k0 + kc : rend - 1;  // padded rows: delta 0
+      float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (fl < F) b4 = __ldg(reinterpret_cast<const float4*>(phi + row * ld + fl));
+      const double b[4] = {(double)b4.x, (double)b4.y, (double)b4.z, (double)b4.w};
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const double a = sd[k0 + kc][t * 8 + n];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[t][j], a, b[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < MT; ++t)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int c = t * 8 + n;
+        const int64_t f = base + 4 * (2 * kc + i) + j;
+        if (c < NC && f < F) dwpart[((int64_t)rs * NC + c) * F + f] = acc[t][j][i];
+      }
+}
+
 template <int NC>
 int launch_bwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
                const HeadScratch& hs, int64_t RS, cudaStream_t st) {
   const int64_t rows_per_split = (m + RS - 1) / RS;
+  if ((F % 4 == 0) && (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0)) {
+    dim3 grid((unsigned)((F + kBDF - 1) / kBDF), (unsigned)RS);
+    return launch_pdl(k_head_bwd_dmma<NC>, grid, dim3(256), 0, st, "k_head_bwd_dmma", phi, m, F, ld,
+                      delta, rows_per_split, hs.dwpart);
+  }
   dim3 grid((unsigned)((F + kBwdK - 1) / kBwdK), (unsigned)RS);
   MCK_TRY(launch_pdl(k_head_bwd<NC>, grid, dim3(kBwdThreads), 0, st, "k_head_bwd", phi, m, F, ld, delta,
                      rows_per_split, hs.dwpart));
