@@ -2,14 +2,15 @@
 // linear_model.py:95-142: forward_batch, loss, gradients, sgd_step).
 //
 // The head is a 10-class contraction over 16,384 features -- a tall-skinny
-// GEMM bound by reading phi (kept L2-resident by the training step), not by
-// math.  It runs on CUDA cores in float64 like the reference (float64 W,
-// logits and gradients over float32 features).  Register blocking: a warp
-// carries 4 rows x C classes of partial logits over a 1,024-feature chunk
-// whose W slice sits in shared memory (forward); a thread carries 4 features
-// x C classes of dW over a row range with delta in shared memory (backward).
-// Every reduction (split-K logits, row splits of dW, db, loss, hits) runs in a
-// fixed order, so training is bit-reproducible.
+// GEMM.  It computes in float64 like the reference (float64 W, logits and
+// gradients over float32 features).  Both contractions run on the FP64
+// tensor cores (mma.sync.m8n8k4.f64) when the feature rows are float4
+// aligned: the forward with 8 rows per warp over 512-feature chunks whose W
+// slice sits in shared memory, the backward with dW tiles of 8 classes x 8
+// features over row splits with delta in shared memory.  CUDA-core fallbacks
+// (k_head_fwd / k_head_bwd) cover unaligned inputs.  Every reduction
+// (split-K logits, row splits of dW, db, loss, hits) runs in a fixed order,
+// so training is bit-reproducible.
 #include <type_traits>
 
 #include "mck_common.cuh"
