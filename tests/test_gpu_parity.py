@@ -390,12 +390,16 @@ class TestFeatures:
 
 # ---------------------------------------------------------------- softmax head / training
 class TestHead:
-    def test_forward_gradients_vs_oracle(self, cuda):
+    # F = 704: FP64-MMA forward with a partial 512-feature chunk (12 groups:
+    # the 8-group loop and the remainder loop); 700: CUDA-core forward,
+    # FP64-MMA backward; 702: both CUDA-core fallbacks (rows not float4)
+    @pytest.mark.parametrize("F", [704, 700, 702])
+    def test_forward_gradients_vs_oracle(self, cuda, F):
         import paper_1702_08159_b200 as P
         rng = np.random.default_rng(4)
-        x = rng.standard_normal((300, 700)).astype(np.float32)
+        x = rng.standard_normal((300, F)).astype(np.float32)
         y = rng.integers(0, 10, 300)
-        w = rng.standard_normal((10, 700)) * 0.05
+        w = rng.standard_normal((10, F)) * 0.05
         b = rng.standard_normal(10) * 0.1
         model = P.SoftmaxModel(w, b)
         np.testing.assert_allclose(P.forward_batch(model, x).cpu().numpy(),
