@@ -2,15 +2,15 @@
 // (BASELINE config 4: d = n = 16384, E = 32, 2^20 features per row, 10
 // classes).  Features are never written to HBM:
 //
-//   for each group of 4 blocks: k_fastfood (z of those blocks only,
-//                         fastfood_z_blocks) -> z tile (m x 4n fp32, scratch)
+//   for each group of 16 blocks: k_fastfood (z of those blocks only,
+//                         fastfood_z_blocks) -> z tile (m x 16n fp32, scratch)
 //                       k_fused_fwd_tc: cos/sin computed on chip from z,
 //                         contracted with the group's W columns on the
 //                         tensor cores into per-chunk partial logits
 //                       k_fused_fold: partial logits -> float64 logits
 //                         (fixed order: groups ascending, chunks in order)
 //   softmax / loss / delta (classifier.cu, k_head_softmax)
-//   for each group of 4 blocks: k_fastfood again (recompute z; cheaper than
+//   for each group of 16 blocks: k_fastfood again (recompute z; cheaper than
 //                         storing 2^20 features per row)
 //                       k_fused_bwd_tc: dW columns of the group = delta^T
 //                         [cos z | sin z] with cos/sin on chip, written or
@@ -36,11 +36,14 @@ int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const d
                              double* rowloss, int32_t* rowhit, cudaStream_t st);
 
 constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
-// Blocks whose z the producer computes per launch: (row, block) items fill
-// the producer's waves better (1,024 rows x 4 blocks over 296 CTA slots:
-// 13.8 of 14 waves instead of 3.5 of 4) and cut its launches 4x; the tile
-// (m x kFusedZBlocks*n) is read back by the contractions from L2/HBM.
-constexpr int kFusedZBlocks = 4;
+// Blocks whose z the producer computes per launch.  (row, block) items fill
+// the producer's waves (1,024 rows x 16 blocks over 296 CTA slots: 55.4 of 56
+// waves), one contraction launch covers the group (2,048 CTAs: 6.9 of 7
+// waves) and launches drop 16x.  The z tile (m x 16n fp32: 1 GiB at m =
+// 1,024, n = 16,384) is scratch in HBM; the features themselves (twice the
+// size of z) are never written.  Measured c4 step: 1 block 6.42 ms, 4 blocks
+// 5.02, 8 blocks 4.80, 16 blocks 4.70, 32 blocks 6.07.
+constexpr int kFusedZBlocks = 16;
 int64_t fused_tc_ksplits(int64_t n);  // fused_tc.cu
 constexpr int kFwarps = 8;
 constexpr int kFrowsPerWarp = 4;
