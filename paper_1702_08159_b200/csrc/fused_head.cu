@@ -168,8 +168,16 @@ k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C, doub
   const int64_t t = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
   if (t < mc) {
-#pragma unroll 4
-    for (int64_t k = w; k < KS; k += kFoldWarps) s += (double)lpart[k * mc + t];
+    // sixteen loads in flight per thread, summed in ascending k
+    int64_t k = w;
+    for (; k + 15 * kFoldWarps < KS; k += 16 * kFoldWarps) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = lpart[(k + i * kFoldWarps) * mc + t];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += (double)v[i];
+    }
+    for (; k < KS; k += kFoldWarps) s += (double)lpart[k * mc + t];
   }
   part[w][lane] = s;
   __syncthreads();
