@@ -464,9 +464,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
   const int64_t units = groups * p.E;
   const int64_t u_lo = units * blockIdx.x / gridDim.x, u_hi = units * (blockIdx.x + 1) / gridDim.x;
-  pdl_wait();
-  pdl_trigger();
-  if (u_lo >= u_hi) return;
+  if (u_lo >= u_hi) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
   const int e_first = (int)(u_lo / groups), e_last = (int)((u_hi - 1) / groups);
   auto issue_tab = [&](int e, int slot) {  // thread 0 only
     const int eg = p.e0 + e;
@@ -497,10 +499,14 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
     fence_mbar_init();
   }
   __syncthreads();
+  // the factor tables are constant for the launch: their copies overlap the
+  // predecessor's tail; x and the output wait for it (pdl_wait)
   if (threadIdx.x == 0) {
     issue_tab(e_first, 0);
     if (e_last > e_first) issue_tab(e_first + 1, 1);
   }
+  pdl_wait();
+  pdl_trigger();
   if constexpr (VEC) {
     if (lane == 0) issue_x(u_lo % groups);
   }
