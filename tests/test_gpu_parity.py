@@ -453,3 +453,28 @@ class TestHostStreaming:
             out.zero_()
             hs.run(x, out)
             assert torch.equal(out, want)
+
+    def test_concurrent_streams_match_sequential(self, cuda):
+        # every entry point is stream-ordered on the caller's stream and
+        # re-entrant: two specs on two streams at once, each with programmatic
+        # dependent launches back to back, give the sequential results bit for bit
+        import paper_1702_08159_b200 as P
+        torch = cuda
+        specs = [P.FeatureMapSpec(784, 6, P.RBF(1.0), 7), P.FeatureMapSpec(300, 3, P.RBFMatern(2.0, 3), 9)]
+        blocks = [P.build_blocks(s) for s in specs]
+        xs = [torch.from_numpy(synthetic.image_rows(1000, s.input_dim, 3 + i)).cuda() for i, s in enumerate(specs)]
+        want = [P.feature_map_batch(s, b, x) for s, b, x in zip(specs, blocks, xs)]
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+        outs = [torch.empty_like(w) for w in want]
+        for rep in range(3):
+            for o in outs:
+                o.zero_()
+            torch.cuda.synchronize()
+            for i in range(2):
+                with torch.cuda.stream(streams[i]):
+                    for _ in range(4):
+                        P.feature_map_batch(specs[i], blocks[i], xs[i], out=outs[i])
+            torch.cuda.synchronize()
+            for o, w in zip(outs, want):
+                assert torch.equal(o, w)
