@@ -14,10 +14,19 @@ needed).  Multi-GPU: every rank expands its own 60,000-row shard (weak
 scaling, no collective on the data path); value = all ranks' features / max
 rank time.
 
-Extras on the single-GPU run: the config-1 FWHT sweep (GB/s per length),
-config 0 (1000-row batch) and one config-3 training epoch.
---impl reference times the reference algorithm (the numpy oracle port of
-mckernel, tests-pinned bit-exact to the reference) on this host's cores.
+`--gpus N` without torchrun re-launches itself under
+`torch.distributed.run` with N local ranks (NCCL, 127.0.0.1).
+
+Extras (every rank, barrier + max-over-ranks device time; each with its
+roofline and, at N = 1 on rank 0, the reference CPU path on the host cores):
+c0 steady state (graph replay of back-to-back 1,000-row batches), the c1
+FWHT sweep (rows of each length split over the ranks), c3 training (step
+time, 20 epochs to the final accuracy; batches sharded + NCCL all-reduce at
+N > 1) and the c4 fused training step (1,024 rows per rank of the 8,192-row
+batch; bucketed all-reduce at N > 1) with its FP32 lane-op and MUFU
+fractions.  --impl reference times the reference algorithm (the numpy oracle
+port of mckernel, tests-pinned bit-exact to the reference) on this host's
+cores.
 """
 
 from __future__ import annotations
@@ -104,10 +113,46 @@ def dist_setup(backend):
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     if ws > 1:
+        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend)
+        # communicator log on stderr (ranks, channels, NVLS) for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group(backend, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, local, ws
+
+
+def comm_info(ws):
+    if ws == 1:
+        return None
+    import torch
+    import torch.distributed as dist
+    v = torch.cuda.nccl.version() if hasattr(torch.cuda, "nccl") else None
+    return {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+            "nccl_version": ".".join(map(str, v)) if isinstance(v, tuple) else v}
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: start N local ranks under torch.distributed.run."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def barrier(ws):
@@ -141,6 +186,8 @@ def bench_ours(args):
 
     rank, local, ws = dist_setup("nccl")
     torch.cuda.set_device(local)
+    if rank == 0 and ws > 1:
+        print(f"[bench] world_size={ws} backend=nccl", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     hbm, peak_kind, peak_json = peaks()
 
@@ -257,10 +304,14 @@ def bench_ours(args):
                    "parallelism": f"row shards x{ws} (no collective)"},
         "roofline": roofline, "e2e": e2e, "gpu_launches": args.steps * len(spans),
         "clocks": clk.summary(), "setup_s": {"build_blocks_c2": round(setup_s, 4)},
+        "comm": comm_info(ws),
     }
-    if ws == 1 and rank == 0 and not args.no_extras:
-        line["extras"] = extras(args, P, torch, dev, hbm)
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    cpu = rank == 0 and ws == 1 and not args.no_cpu
+    if not args.no_extras:
+        del out
+        torch.cuda.empty_cache()
+        line["extras"] = extras(args, P, torch, dev, hbm, rank, ws, cpu)
+    if cpu:
         line["cpu_baseline"] = cpu_baseline_c2(sample_rows=args.cpu_rows, reps=2)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -269,96 +320,280 @@ def bench_ours(args):
         dist.destroy_process_group()
 
 
-def time_cuda(fn, reps, torch, stream=None):
+def timed(fn, reps, torch, ws, dev, stream=None):
+    """ms per call: barrier + synchronize on both sides, CUDA events on the
+    launching stream, max over ranks."""
+    stream = stream or torch.cuda.current_stream(dev)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(ws)
     torch.cuda.synchronize()
-    s.record()
+    s.record(stream)
     for _ in range(reps):
         fn()
-    e.record()
+    e.record(stream)
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / reps
+    barrier(ws)
+    return max_over_ranks(s.elapsed_time(e) / reps, ws, dev)
 
 
-def extras(args, P, torch, dev, hbm):
-    import numpy as np
+def sm_clock_hz():
+    _, _, pj = peaks()
+    return float(pj.get("sm_max_mhz", 1965.0)) * 1e6
+
+
+def extras(args, P, torch, dev, hbm, rank, ws, cpu):
+    """Per-config legs, each with a roofline and (N=1,
+    rank 0) the reference CPU path.  Every rank runs every leg; times are the
+    max over ranks; values are whole-job aggregates."""
     from paper_1702_08159_b200 import synthetic
+    from paper_1702_08159_b200.distributed import shard_range
     out = {}
-    # config 1: FWHT sweep, 2^28 floats (1 GiB) per length, in place; GB/s on
-    # algorithmic bytes (read + write once = 2^31 B)
-    sweep = {}
-    g = torch.Generator(device=dev).manual_seed(7)
-    buf = torch.randn(1 << 28, generator=g, device=dev)
-    for k in range(10, 21):
-        n = 1 << k
-        mat = buf.view(-1, n)
-        P.wht_fast_batch(mat)
-        ms = time_cuda(lambda: P.wht_fast_batch(mat), 5, torch)
-        sweep[str(n)] = {"ms": round(ms, 4), "GBps": round(2 ** 31 / (ms / 1e3) / 1e9, 1),
-                         "frac": round(2 ** 31 / (ms / 1e3) / 1e9 / hbm, 4)}
-    del buf
-    out["c1_fwht_sweep"] = sweep
-    # config 0: 1000 x 784, RBF E=8 -> 16384 features/row (launch-latency sized)
+    cores = os.cpu_count() or 1
+
+    # ---- config 0: RBF E=8, 1000 x 784 -> 16384 features/row.  Steady state:
+    # 20 back-to-back batches replayed from one CUDA graph; 4 rotating output
+    # buffers (262 MB > L2) so no write is absorbed by L2.
     spec0 = P.FeatureMapSpec(784, 8, P.RBF(1.0), 1234)
     b0 = P.build_blocks(spec0)
-    x0 = torch.from_numpy(synthetic.image_rows(1000, 784, 1234)).to(dev)
-    o0 = torch.empty((1000, 16384), device=dev)
-    P.feature_map_batch(spec0, b0, x0, out=o0)
-    ms0 = time_cuda(lambda: P.feature_map_batch(spec0, b0, x0, out=o0), 50, torch)
-    out["c0_features"] = {"ms_per_batch": round(ms0, 4),
-                          "features_per_s": 1000 * 16384 / (ms0 / 1e3),
-                          "GBps": round(1000 * (3136 + 65536) / (ms0 / 1e3) / 1e9, 1)}
-    # config 4 expansion alone (n = 16384, E = 32, sigma = 4): 256 rows ->
-    # 2^20 features/row materialised (the fused classifier path is K6)
+    x0 = torch.from_numpy(synthetic.image_rows(1000, 784, 1234 + rank)).to(dev)
+    o0 = [torch.empty((1000, 16384), device=dev) for _ in range(4)]
+    P.feature_map_batch(spec0, b0, x0, out=o0[0])
+    one_ms = timed(lambda: P.feature_map_batch(spec0, b0, x0, out=o0[0]), 50, torch, ws, dev)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for k in range(20):
+            P.feature_map_batch(spec0, b0, x0, out=o0[k % 4])
+    graph.replay()
+    g_ms = timed(graph.replay, 10, torch, ws, dev) / 20
+    bpr0 = 784 * 4 + 16384 * 4
+    gbs0 = 1000 * bpr0 / (g_ms / 1e3) / 1e9
+    out["c0"] = {"workload": "RBF sigma=1, E=8, 1000x784 -> 16384 features/row per rank",
+                 "ms_per_batch_single_launch": round(one_ms, 4),
+                 "ms_per_batch_steady": round(g_ms, 4),
+                 "features_per_s": ws * 1000 * 16384 / (g_ms / 1e3),
+                 "roofline": {"bound": "hbm", "kernel": "k_fastfood_pair (n=1024)",
+                              "achieved": round(gbs0, 1), "peak": hbm, "unit": "GB/s",
+                              "frac": round(gbs0 / hbm, 4),
+                              "alg_bytes_per_batch": 1000 * bpr0,
+                              "method": "graph of 20 back-to-back batches, 4 rotating outputs"}}
+    del o0, graph
+    if cpu:
+        out["c0"]["cpu_baseline"] = cpu_features(spec0, synthetic.image_rows(1000, 784, 1234), cores)
+
+    # ---- config 1: FWHT sweep, 2^28 floats (1 GiB) per length in place, rows
+    # split over the ranks; GB/s on algorithmic bytes (read + write once).
+    sweep = {}
+    total = 1 << 28
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    buf = torch.randn(total // ws + (1 << 20), generator=g, device=dev)
+    for k in range(10, 21):
+        n = 1 << k
+        rows = total // n
+        lo, hi = shard_range(rows, rank, ws)
+        mat = buf[:(hi - lo) * n].view(-1, n) if hi > lo else None
+        fn = (lambda: P.wht_fast_batch(mat)) if mat is not None else (lambda: None)
+        fn()
+        ms = timed(fn, 5, torch, ws, dev)
+        gbs = 2 ** 31 / (ms / 1e3) / 1e9
+        kern = ("fwht_rows_kernel" if k <= 14 else "fwht_cluster_kernel" if k <= 17
+                else "two-phase (columns + rows)")
+        sweep[str(n)] = {"ms": round(ms, 4), "GBps": round(gbs, 1), "frac": round(gbs / hbm, 4),
+                         "rows_per_rank": hi - lo, "kernel": kern}
+    del buf
+    if cpu:
+        cpu_sweep = cpu_wht_sweep(cores)
+        for n, v in cpu_sweep.items():
+            sweep[n]["cpu_baseline"] = v
+    out["c1_fwht_sweep"] = sweep
+
+    # ---- config 4: fused expansion -> classifier training step, 1024 rows per
+    # rank of the 8192-row global batch (features never in HBM).
+    from paper_1702_08159_b200.large_scale import FusedClassifier
     spec4 = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4)
     t0 = time.perf_counter()
-    b4 = P.build_blocks(spec4)
+    fc = FusedClassifier(spec4, 10, 1024)
     torch.cuda.synchronize()
     setup4 = time.perf_counter() - t0
-    x4 = torch.randn((256, 16384), generator=torch.Generator(device=dev).manual_seed(7),
+    x4 = torch.randn((1024, 16384), generator=torch.Generator(device=dev).manual_seed(7 + rank),
                      device=dev)
-    o4 = torch.empty((256, 1 << 20), device=dev)
-    P.feature_map_batch(spec4, b4, x4, normalize=False, out=o4)
-    ms4 = time_cuda(lambda: P.feature_map_batch(spec4, b4, x4, normalize=False, out=o4), 5, torch)
-    out["c4_expansion"] = {"rows": 256, "ms": round(ms4, 4),
-                           "features_per_s": 256 * (1 << 20) / (ms4 / 1e3),
-                           "GBps": round(256 * (65536 + 4 * (1 << 20)) / (ms4 / 1e3) / 1e9, 1),
-                           "build_blocks_s": round(setup4, 3)}
-    del o4, x4
-    # config 4 fused training step (K6): one rank's 1024-row shard of the
-    # 8192-row global batch; forward + backward (expansion recomputed) + SGD,
-    # features never written to HBM
-    from paper_1702_08159_b200.large_scale import FusedClassifier
-    fc = FusedClassifier(spec4, 10, 1024)
-    x4 = torch.randn((1024, 16384), generator=torch.Generator(device=dev).manual_seed(7),
-                     device=dev)
-    y4 = torch.randint(0, 10, (1024,), device=dev, dtype=torch.int32)
-    fc.step(x4, y4, m_total=8192, lr=0.01)
-    ms_step = time_cuda(lambda: fc.step(x4, y4, m_total=8192, lr=0.01), 3, torch)
-    out["c4_fused_step"] = {"rows_per_rank": 1024, "global_batch": 8192, "ms_per_step": round(ms_step, 3),
-                            "features_per_s": 1024 * (1 << 20) / (ms_step / 1e3),
-                            "note": "forward+backward+update; features_per_s counts each row's 2^20 "
-                                    "features once per step"}
-    del fc, x4
-    # config 3: one training epoch (60 steps of 1000 rows + 10k-row evaluation)
+    y4 = torch.randint(0, 10, (1024,), device=dev, dtype=torch.int32,
+                       generator=torch.Generator(device=dev).manual_seed(8 + rank))
+    mt = 8192 if ws <= 8 else 1024 * ws          # global batch; this rank's shard is 1024 rows
+    for _ in range(2):
+        fc.step(x4, y4, m_total=mt, lr=0.01)
+    ms4 = timed(lambda: fc.step(x4, y4, m_total=mt, lr=0.01), 5, torch, ws, dev)
+    n4, E4, rows4 = 16384, 32, 1024
+    # algorithmic lane work per step: two expansions (forward, backward recompute)
+    # of every (row, block): 2 FWHTs x (n/2 log2 n butterflies x 2 add/sub)
+    # + G and C multiplies; MUFU: cos and sin of every z in both passes.
+    lane_ops = 2 * rows4 * E4 * (2 * (n4 // 2) * 14 * 2 + 2 * n4)
+    mufu = 2 * rows4 * E4 * 2 * n4
+    f_sm = sm_clock_hz()
+    lane_peak = 148 * 128 * f_sm
+    mufu_peak = 148 * 16 * f_sm
+    ach_l = lane_ops / (ms4 / 1e3)
+    ach_m = mufu / (ms4 / 1e3)
+    out["c4_fused_step"] = {
+        "workload": "RBF sigma=4, n=d=16384, E=32 -> 2^20 features/row, 10 classes; "
+                    "1024 rows per rank of the 8192-row global batch; fwd + bwd (recomputed "
+                    "expansion) + SGD, features never written to HBM",
+        "rows_per_rank": rows4, "ms_per_step": round(ms4, 3),
+        "features_per_s": ws * rows4 * (1 << 20) / (ms4 / 1e3),
+        "build_blocks_s": round(setup4, 3),
+        "allreduce": (f"{len(fc.bucket_ranges())} float32 buckets of {fc.bucket_blocks} blocks "
+                      f"(+ float64 [db|loss|hits]), overlapped with the backward" if ws > 1 else None),
+        "roofline": {"bound": "fp32 lanes / MUFU", "unit": "op/s",
+                     "lane_ops_per_step": lane_ops, "achieved": ach_l, "peak": lane_peak,
+                     "frac": round(ach_l / lane_peak, 4),
+                     "mufu_per_step": mufu, "mufu_achieved": ach_m, "mufu_peak": mufu_peak,
+                     "mufu_frac": round(ach_m / mufu_peak, 4),
+                     "peak_source": "148 SMs x 128 FP32 lanes (16 MUFU/clk) x sm_max_mhz; "
+                                    "packed f32x2 ops counted as 2"}}
+    if cpu:
+        out["c4_fused_step"]["cpu_baseline"] = cpu_c4(spec4, fc, x4, y4, cores)
+    del fc, x4, y4
+    torch.cuda.empty_cache()
+
+    # ---- config 3: end-to-end SGD, 60000 x 784, RBF E=8, batch 1000, lr 0.01,
+    # 20 epochs; every global batch sharded over the ranks.
     x, y = synthetic.class_images(60000, 784, 10, seed=1234)
     xt, yt = synthetic.class_images(10000, 784, 10, seed=1234, sample_seed=99)
-    cfg = P.TrainConfig(0.01, 1000, 2)
+    cfg = P.TrainConfig(0.01, 1000, 20)
     tr = P.Trainer(spec0, P.Dataset(x, y, 10), P.Dataset(xt, yt, 10), cfg)
-    for s in range(tr.steps):
-        tr.step(0, s)
-    torch.cuda.synchronize()
-    t_steps = time_cuda(lambda: [tr.step(1, s) for s in range(tr.steps)], 1, torch)
-    tr.evaluate()  # first call allocates the evaluation buffers
+    tr.run_epoch(0)
+    ms_epoch = timed(lambda: tr.run_epoch(1), 1, torch, ws, dev)
+    tr.evaluate()
+    barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    tr.evaluate()  # returns host scalars (synchronises)
-    t_eval = (time.perf_counter() - t0) * 1e3
-    out["c3_train"] = {"ms_per_epoch_steps": round(t_steps, 3), "ms_eval": round(t_eval, 3),
-                       "ms_per_step": round(t_steps / tr.steps, 4),
-                       "features_per_s": 60000 * 16384 / (t_steps / 1e3),
-                       "epoch_loss": tr.epoch_loss()}
+    model, metrics = P.train(spec0, P.Dataset(x, y, 10), P.Dataset(xt, yt, 10), cfg)
+    t20 = max_over_ranks(time.perf_counter() - t0, ws, dev)
+    step_ms = ms_epoch / tr.steps
+    c3_bytes = 1000 * (784 * 4 + 3 * 16384 * 4)   # x once; phi written, read by fwd and bwd
+    gbs3 = c3_bytes / (step_ms / 1e3) / 1e9
+    out["c3_train"] = {
+        "workload": "60000x784 10-class synthetic, RBF sigma=1 E=8 (16384 features), softmax "
+                    "head, batch 1000, lr 0.01, 20 epochs; eval on 10000 rows each epoch",
+        "ms_per_step": round(step_ms, 4), "ms_per_epoch_steps": round(ms_epoch, 3),
+        "features_per_s": 60000 * 16384 / (ms_epoch / 1e3),
+        "time_to_20_epochs_s": round(t20, 3),
+        "final_test_acc": metrics.records[-1].test_acc,
+        "final_train_loss": metrics.records[-1].train_loss,
+        "loss_history": [round(r.train_loss, 6) for r in metrics.records],
+        "roofline": {"bound": "hbm", "achieved": round(gbs3, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(gbs3 / hbm, 4), "alg_bytes_per_step": c3_bytes,
+                     "note": "x rows once + phi (65.5 MB) written and read by the forward and "
+                             "backward (SURVEY 8d, ~200 MB/step); the step is latency-bound"}}
+    if cpu:
+        out["c3_train"]["cpu_baseline"] = cpu_c3(spec0, x, y, cores)
     return out
+
+
+def cpu_features(spec, x, cores, reps=2):
+    """Reference feature_map_batch (oracle port) over a thread pool, BLAS 1 thread."""
+    import concurrent.futures as cf
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import fastfood as off
+    ospec = off.OSpec.of(spec)
+    with threadpool_limits(1):
+        blocks = off.build_blocks(ospec)
+        chunks = [c for c in np.array_split(x, 4 * cores) if len(c)]
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            with cf.ThreadPoolExecutor(cores) as ex:
+                list(ex.map(lambda c: off.feature_map_batch(ospec, blocks, c), chunks))
+            times.append(time.perf_counter() - t0)
+    return {"value": len(x) * 2 * ospec.n * ospec.expansions / min(times), "unit": "features/s",
+            "cores": cores, "kind": "port",
+            "sample": f"all {len(x)} rows, ThreadPool x{cores}, 1 BLAS thread, best of {reps}"}
+
+
+def cpu_wht_sweep(cores, floats=1 << 22):
+    """Reference wht_fast_batch (oracle port) per length on `floats` floats."""
+    import concurrent.futures as cf
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import wht as ow
+    res = {}
+    rng = np.random.default_rng(7)
+    base = rng.standard_normal(floats).astype(np.float32)
+    with threadpool_limits(1):
+        for k in range(10, 21):
+            n = 1 << k
+            mat = base.copy().reshape(-1, n)
+            chunks = [c for c in np.array_split(mat, min(cores, mat.shape[0])) if len(c)]
+            best = None
+            for _ in range(2):
+                parts = [np.ascontiguousarray(c) for c in chunks]
+                t0 = time.perf_counter()
+                with cf.ThreadPoolExecutor(len(parts)) as ex:
+                    list(ex.map(ow.wht_fast_batch, parts))
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+            res[str(n)] = {"GBps": round(floats * 8 / best / 1e9, 3), "cores": len(chunks),
+                           "kind": "port", "sample": f"{floats} floats ({mat.shape[0]} rows)"}
+    return res
+
+
+def cpu_c3(spec, x, y, cores, steps=3):
+    """Reference train step (oracle port: featurize, loss, sgd_step -- the
+    forward runs twice, linear_model.py:218-219) with BLAS on all cores;
+    extrapolated to s/epoch (60 steps) and 20 epochs."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import fastfood as off
+    from oracle import linear_model as olm
+    ospec = off.OSpec.of(spec)
+    blocks = off.build_blocks(ospec)
+    w, b = np.zeros((10, 16384)), np.zeros(10)
+    order = olm.epoch_order(0, 0, len(y))
+    times = []
+    with threadpool_limits(cores):
+        for s in range(steps):
+            idx = order[s * 1000:(s + 1) * 1000]
+            t0 = time.perf_counter()
+            xb = off.feature_map_batch(ospec, blocks, x[idx], normalize=False)
+            olm.loss(w, b, xb, y[idx])
+            olm.sgd_step(w, b, xb, y[idx], 0.01)
+            times.append(time.perf_counter() - t0)
+    st = float(np.median(times))
+    return {"value": 1000 * 16384 / st, "unit": "features/s", "cores": cores, "kind": "port",
+            "s_per_step": round(st, 4), "s_per_epoch": round(60 * st, 2),
+            "time_to_20_epochs_s": round(1200 * st, 1),
+            "sample": f"{steps} steps of 1000 rows (median), BLAS threads = {cores}; "
+                      "evaluation excluded"}
+
+
+def cpu_c4(spec, fc, x4, y4, cores, rows=4):
+    """Reference path for config 4 on a sample: featurize `rows` rows through
+    all 32 blocks (materialised, as the reference must), loss + sgd_step on
+    them; extrapolated to one rank's 1024-row step.  The factor tables are the
+    product's (identical to the reference's; building C-RBF on the CPU takes
+    ~30 s per block), which does not change the timed work."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle import fastfood as off
+    from oracle import linear_model as olm
+    ospec = off.OSpec.of(spec)
+    blocks = [off.OBlock(*fc.blocks[e].numpy(), e) for e in range(spec.expansions)]
+    x = x4[:rows].cpu().numpy()
+    y = y4[:rows].cpu().numpy().astype(np.int64)
+    w, b = np.zeros((10, 1 << 20)), np.zeros(10)
+    with threadpool_limits(cores):
+        t0 = time.perf_counter()
+        xb = off.feature_map_batch(ospec, blocks, x, normalize=False)
+        olm.loss(w, b, xb, y)
+        olm.sgd_step(w, b, xb, y, 0.01)
+        dt = time.perf_counter() - t0
+    per_row = dt / rows
+    return {"value": rows * (1 << 20) / dt, "unit": "features/s", "cores": cores, "kind": "port",
+            "s_per_rank_step_extrapolated": round(per_row * 1024, 2),
+            "sample": f"{rows} rows x 32 blocks (n=16384), featurize + loss + sgd_step, "
+                      f"extrapolated x{1024 // rows} to a 1024-row rank step"}
 
 
 # ------------------------------------------------------------------ CPU / reference
@@ -387,7 +622,7 @@ def cpu_baseline_c2(sample_rows=4096, reps=2, warmup=0, steps=None):
             blocks = pool.starmap(off.build_block, [(ospec, e) for e in range(ospec.expansions)])
     build_s = time.perf_counter() - t0
     x = synthetic.image_rows(C2["rows"], C2["d"], C2["xseed"])[:sample_rows]
-    chunks = np.array_split(x, 4 * cores)
+    chunks = [c for c in np.array_split(x, 4 * cores) if len(c)]
 
     def run():
         with cf.ThreadPoolExecutor(cores) as ex:
@@ -447,6 +682,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

@@ -180,6 +180,30 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t expansions
                        float* w, double* b, double lr, double l2, void* scratch,
                        int32_t variant, void* stream);
 
+/* Multi-rank backward, one all-reduce bucket at a time (SURVEY.md 8(e) c4:
+ * buckets by block, overlapped with the rest of the backward).  dW of the
+ * blocks [e_begin, e_begin + e_count) is written to bucket as float32
+ * [C][cos columns of the range | sin columns of the range]
+ * (C * 2 * e_count * n floats, contiguous), to be summed over ranks and then
+ * applied with mck_fused_apply_bucket.  Replaces the dW half of
+ * linear_model.py:118-131 for a slice of W's columns. */
+int mck_fused_backward_bucket(const void* tables, int64_t input_dim, int32_t expansions,
+                              double sigma, const float* x, int64_t m, int64_t ldx,
+                              const int32_t* row_index, const double* delta, int32_t num_classes,
+                              int32_t e_begin, int32_t e_count, float* bucket, void* scratch,
+                              int32_t variant, void* stream);
+
+/* db = sum_r delta_r (float64, C values) -- linear_model.py:130. */
+int mck_fused_bias_grad(const double* delta, int64_t m, int32_t num_classes, double* db,
+                        void* stream);
+
+/* W[:, columns of blocks e_begin..] -= lr * (bucket + 2*l2*W) (float32) and,
+ * if b != NULL, b -= lr * db (float64) -- linear_model.py:134-142 applied to
+ * an all-reduced bucket. */
+int mck_fused_apply_bucket(float* w, int64_t input_dim, int32_t expansions, int32_t num_classes,
+                           int32_t e_begin, int32_t e_count, const float* bucket, double lr,
+                           double l2, double* b, const double* db, void* stream);
+
 /* -------------------------------------------------------------- diagnostics */
 /* tcgen05 self-test: D (128 x 16) = A (128 x K) * B (16 x K)^T, kind::tf32,
  * operands via shared memory, accumulator in TMEM (K % 8 == 0, K <= 256). */

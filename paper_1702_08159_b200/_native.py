@@ -53,6 +53,11 @@ SIGNATURES: dict[str, tuple] = {
                                     _p, _i64, _p, _p, _p, _p, _p, _p, _i32, _p]),
     "mck_fused_backward": (C.c_int, [_p, _i64, _i32, _f64, _p, _i64, _i64, _p, _p, _i32, _p, _p,
                                      _p, _p, _f64, _f64, _p, _i32, _p]),
+    "mck_fused_backward_bucket": (C.c_int, [_p, _i64, _i32, _f64, _p, _i64, _i64, _p, _p, _i32,
+                                            _i32, _i32, _p, _p, _i32, _p]),
+    "mck_fused_bias_grad": (C.c_int, [_p, _i64, _i32, _p, _p]),
+    "mck_fused_apply_bucket": (C.c_int, [_p, _i64, _i32, _i32, _i32, _i32, _p, _f64, _f64, _p, _p,
+                                         _p]),
     "mck_diag_umma_tf32": (C.c_int, [_p, _p, _p, _i32, _p]),
     "mck_diag_edge_color32": (C.c_int, [_i32, _p, _p, _p]),
 }

@@ -69,6 +69,12 @@ int fused_forward(const TablesView&, int32_t, double, const float*, int64_t, int
 int fused_backward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
                    const int32_t*, const double*, int32_t, float*, double*, float*, double*,
                    double, double, void*, int32_t, cudaStream_t);
+int fused_backward_range(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
+                         const int32_t*, const double*, int32_t, int32_t, int32_t, float*, int64_t,
+                         int64_t, int64_t, float*, double, double, void*, int32_t, cudaStream_t);
+int fused_bias_grad(const double*, int64_t, int32_t, double*, cudaStream_t);
+int fused_apply_bucket(float*, int64_t, int32_t, int32_t, int32_t, int32_t, const float*, double, double,
+                       double*, const double*, cudaStream_t);
 
 static bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 static int64_t next_pow2(int64_t d) {
@@ -309,6 +315,45 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double 
   tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
   return fused_backward(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, delta, C, dw, db, w,
                         b, lr, l2, scratch, variant, S(st));
+}
+
+int mck_fused_backward_bucket(const void* tables, int64_t input_dim, int32_t E, double sigma,
+                              const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
+                              const double* delta, int32_t C, int32_t e_begin, int32_t e_count,
+                              float* bucket, void* scratch, int32_t variant, void* st) {
+  const int64_t n = next_pow2(input_dim);
+  MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
+  if (e_begin < 0 || e_count < 1 || e_begin + e_count > E)
+    return fail_value("block range [%d, %d) outside 0..%d", e_begin, e_begin + e_count, E);
+  if (!bucket || (m > 0 && (!delta || !scratch))) return fail_value("NULL argument");
+  if (C < 2 || C > 16) return fail_value("num_classes must be in 2..16");
+  if (m == 0)
+    return check_cuda(cudaMemsetAsync(bucket, 0, (size_t)C * 2 * e_count * n * sizeof(float), S(st)),
+                      "bucket clear");
+  TablesView tv;
+  tables_layout(n, E, (char*)const_cast<void*>(tables), &tv);
+  const int64_t nz = (int64_t)e_count * n;
+  return fused_backward_range(tv, (int32_t)input_dim, sigma, x, m, ldx, row_index, delta, C, e_begin,
+                              e_count, bucket, 2 * nz, 0, nz, nullptr, 0.0, 0.0, scratch, variant, S(st));
+}
+
+int mck_fused_bias_grad(const double* delta, int64_t m, int32_t C, double* db, void* st) {
+  if (C < 2 || C > 16) return fail_value("num_classes must be in 2..16");
+  if (!db || (m > 0 && !delta)) return fail_value("NULL argument");
+  if (m == 0) return check_cuda(cudaMemsetAsync(db, 0, (size_t)C * 8, S(st)), "db clear");
+  return fused_bias_grad(delta, m, C, db, S(st));
+}
+
+int mck_fused_apply_bucket(float* w, int64_t input_dim, int32_t E, int32_t C, int32_t e_begin,
+                           int32_t e_count, const float* bucket, double lr, double l2, double* b,
+                           const double* db, void* st) {
+  if (input_dim < 1 || E < 1) return fail_value("bad spec");
+  if (e_begin < 0 || e_count < 1 || e_begin + e_count > E)
+    return fail_value("block range [%d, %d) outside 0..%d", e_begin, e_begin + e_count, E);
+  if (!(lr > 0.0)) return fail_value("learning rate must be positive");
+  if (!w || !bucket || (b && !db)) return fail_value("NULL argument");
+  if (C < 2 || C > 16) return fail_value("num_classes must be in 2..16");
+  return fused_apply_bucket(w, next_pow2(input_dim), E, C, e_begin, e_count, bucket, lr, l2, b, db, S(st));
 }
 
 }  // extern "C"

@@ -302,12 +302,12 @@ int launch_fwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double*
     constexpr int NT = (NC + 7) / 8;
     const size_t smem = (size_t)NT * 8 * kDStride * sizeof(double);
     auto kern = k_head_fwd_dmma<NC>;
-    static bool init = false;
-    if (!init) {
-      MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)smem), "head fwd dmma smem"));
-      init = true;
-    }
+    static PerDevice pd;
+    const DeviceSlot* ds = nullptr;
+    MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
+      return check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem), "head fwd dmma smem");
+    }));
     *ksplits = (F + kDK - 1) / kDK;
     dim3 grid((unsigned)((m + kDRows - 1) / kDRows), (unsigned)*ksplits);
     return launch_pdl(kern, grid, dim3(256), smem, st, "k_head_fwd_dmma", phi, m, F, ld, w, partial);

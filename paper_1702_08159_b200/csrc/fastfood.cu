@@ -689,19 +689,18 @@ int launch_ff_pair(const FFParams& p, cudaStream_t st) {
   constexpr int ROWS = 2 * kPairWarps;
   const size_t smem = ff_pair_smem_bytes<C>();
   auto kern = k_fastfood_pair<FEAT, FOLD, VEC>;
-  static int occ = 0, sms = 0;
-  if (occ == 0) {
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot& s) {
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "fastfood pair smem"));
-    int dev = 0;
-    MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
-    MCK_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms"));
-    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPairWarps * 32, smem),
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.occ, kern, kPairWarps * 32, smem),
                        "occupancy"));
-    if (occ < 1) occ = 1;
-  }
+    if (s.occ < 1) s.occ = 1;
+    return MCK_OK;
+  }));
   const int64_t items = (p.m + ROWS - 1) / ROWS * p.E;
-  int64_t grid = (int64_t)sms * occ;
+  int64_t grid = (int64_t)ds->sms * ds->occ;
   if (grid > items) grid = items;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kPairWarps * 32), smem, st, "k_fastfood_pair", p);
 }
@@ -894,20 +893,19 @@ int launch_ff(const FFParams& p, cudaStream_t st) {
   constexpr int ROWS = ff_rows_per_cta<C>();
   const size_t smem = ff_smem_bytes<C>();
   auto kern = k_fastfood<C, FEAT, FOLD, VEC>;
-  static int occ = 0, sms = 0;  // per instantiation, per process (one device type)
-  if (occ == 0) {
+  static PerDevice pd;  // per instantiation, per device
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot& s) {
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "fastfood smem"));
-    int dev = 0;
-    MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
-    MCK_TRY(check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms"));
-    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::T * ROWS, smem),
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s.occ, kern, C::T * ROWS, smem),
                        "occupancy"));
-    if (occ < 1) occ = 1;
-  }
+    if (s.occ < 1) s.occ = 1;
+    return MCK_OK;
+  }));
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
   const int64_t work = ff_xreg<C>() ? groups : groups * p.E;
-  int64_t grid = (int64_t)sms * occ;
+  int64_t grid = (int64_t)ds->sms * ds->occ;
   if (grid > work) grid = work;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(C::T * ROWS), smem, st, "k_fastfood", p);
 }

@@ -346,12 +346,20 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                                   fs.rowhit, st);
 }
 
-int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
-                   int64_t ldx, const int32_t* rows, const double* delta, int32_t C, float* dw,
-                   double* db, float* w, double* b, double lr, double l2, void* scratch,
-                   int32_t cuda_cores, cudaStream_t st) {
+// Backward of blocks [e_begin, e_begin + e_count) only.  dW of those blocks
+// goes to dw with row stride ldw; block e_begin + k's cos columns start at
+// cos0 + k n and its sin columns at sin0 + k n.  The plain layout is
+// (ldw, cos0, sin0) = (F, e_begin n, D + e_begin n); an all-reduce bucket
+// uses (2 e_count n, 0, e_count n), i.e. [C][cos | sin] of the range,
+// contiguous.  With w != NULL the update is applied in place instead
+// (plain layout only).
+int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                         int64_t ldx, const int32_t* rows, const double* delta, int32_t C,
+                         int32_t e_begin, int32_t e_count, float* dw, int64_t ldw, int64_t cos0,
+                         int64_t sin0, float* w, double lr, double l2, void* scratch,
+                         int32_t cuda_cores, cudaStream_t st) {
   if (m == 0) return MCK_OK;
-  const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
+  const int64_t n = tv.n;
   FusedScratch fs;
   fused_layout(m, n, C, (char*)scratch, &fs);
   const int64_t RS = fused_rsplits(m);
@@ -359,13 +367,15 @@ int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x
   k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
   MCK_TRY(check_launch("k_to_f32"));
   const int64_t ldz = n * kFusedZBlocks;
-  for (int32_t e = 0; e < E; e += kFusedZBlocks) {
-    const int32_t nb = (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks);
+  const int32_t e_end = e_begin + e_count;
+  for (int32_t e = e_begin; e < e_end; e += kFusedZBlocks) {
+    const int32_t nb = (int32_t)(e_end - e < kFusedZBlocks ? e_end - e : kFusedZBlocks);
     const int64_t nz = (int64_t)nb * n;
+    const int64_t cc = cos0 + (int64_t)(e - e_begin) * n, cs = sin0 + (int64_t)(e - e_begin) * n;
     MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, fs.z, ldz, st));
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_tc(fs.z, m, nz, ldz, fs.delta32, C, F, (int64_t)e * n, D + (int64_t)e * n, dw,
-                           w, (float)lr, (float)l2, st));
+      MCK_TRY(fused_bwd_tc(fs.z, m, nz, ldz, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
+                           st));
       continue;
     }
     MCK_TRY(dispatch_nc(C, [&](auto nc) {
@@ -376,13 +386,61 @@ int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x
     }));
     int64_t grid = ((int64_t)C * 2 * nz + 255) / 256;
     if (grid > 148 * 8) grid = 148 * 8;
-    k_fused_dw_finish<<<(unsigned)grid, 256, 0, st>>>(fs.dwpart, RS, C, nz, F, (int64_t)e * n,
-                                                      D + (int64_t)e * n, dw, w, (float)lr,
-                                                      (float)l2);
+    k_fused_dw_finish<<<(unsigned)grid, 256, 0, st>>>(fs.dwpart, RS, C, nz, ldw, cc, cs, dw, w,
+                                                      (float)lr, (float)l2);
     MCK_TRY(check_launch("k_fused_dw_finish"));
   }
+  return MCK_OK;
+}
+
+int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
+                   int64_t ldx, const int32_t* rows, const double* delta, int32_t C, float* dw,
+                   double* db, float* w, double* b, double lr, double l2, void* scratch,
+                   int32_t cuda_cores, cudaStream_t st) {
+  if (m == 0) return MCK_OK;
+  const int64_t n = tv.n, D = n * tv.E, F = 2 * D;
+  MCK_TRY(fused_backward_range(tv, d, sigma, x, m, ldx, rows, delta, C, 0, (int32_t)tv.E, dw, F, 0, D,
+                               w, lr, l2, scratch, cuda_cores, st));
   k_fused_db<<<C, 256, 0, st>>>(delta, m, C, db, b, lr);
   return check_launch("k_fused_db");
+}
+
+int fused_bias_grad(const double* delta, int64_t m, int32_t C, double* db, cudaStream_t st) {
+  k_fused_db<<<C, 256, 0, st>>>(delta, m, C, db, nullptr, 0.0);
+  return check_launch("k_fused_db");
+}
+
+// W[c][block columns] -= lr * (g + 2 l2 W) for the bucket of blocks
+// [e_begin, e_begin + e_count) (layout of fused_backward_range's bucket), and
+// b -= lr * db when b is given.  Same float32 arithmetic as the fused update
+// of the single-rank backward (k_fused_bwd_tc / k_fused_dw_finish).
+__global__ void k_fused_apply_bucket(float* __restrict__ w, int64_t F, int64_t D, int64_t n,
+                                     int32_t e_begin, int64_t nz, int C,
+                                     const float* __restrict__ bucket, float lr, float l2,
+                                     double* __restrict__ b, const double* __restrict__ db,
+                                     double lr64) {
+  const int64_t total = (int64_t)C * 2 * nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / (2 * nz), k = i - c * 2 * nz;
+    const int64_t col = c * F + (k < nz ? (int64_t)e_begin * n + k : D + (int64_t)e_begin * n + (k - nz));
+    const float g = bucket[i];
+    const float wv = w[col];
+    w[col] = wv - lr * (l2 != 0.f ? g + 2.f * l2 * wv : g);
+  }
+  if (b && blockIdx.x == 0 && threadIdx.x < C) b[threadIdx.x] -= lr64 * db[threadIdx.x];
+}
+
+int fused_apply_bucket(float* w, int64_t n, int32_t E, int32_t C, int32_t e_begin, int32_t e_count,
+                       const float* bucket, double lr, double l2, double* b, const double* db,
+                       cudaStream_t st) {
+  const int64_t D = n * E, nz = (int64_t)e_count * n;
+  int64_t grid = ((int64_t)C * 2 * nz + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid < 1) grid = 1;
+  k_fused_apply_bucket<<<(unsigned)grid, 256, 0, st>>>(w, 2 * D, D, n, e_begin, nz, C, bucket,
+                                                       (float)lr, (float)l2, b, db, lr);
+  return check_launch("k_fused_apply_bucket");
 }
 
 }  // namespace mck

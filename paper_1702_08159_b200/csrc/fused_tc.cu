@@ -398,12 +398,12 @@ int fused_fwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float*
                  int64_t col_cos, int64_t col_sin, float* lpart, cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
   const size_t smem = sizeof(FwdSmem);
-  static bool init = false;
-  if (!init) {
-    MCK_TRY(check_cuda(cudaFuncSetAttribute(k_fused_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem), "fwd tc smem"));
-    init = true;
-  }
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
+    return check_cuda(cudaFuncSetAttribute(k_fused_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem), "fwd tc smem");
+  }));
   const int64_t KS = (n + kFzCta - 1) / kFzCta, RT = (m + kTcM - 1) / kTcM;
   // row tiles per CTA: enough CTAs for one wave of 2 per SM, W slice reused
   int64_t per = 296 / KS;
@@ -421,12 +421,12 @@ int fused_bwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float*
                  cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
   const size_t smem = sizeof(BwdSmem);
-  static bool init = false;
-  if (!init) {
-    MCK_TRY(check_cuda(cudaFuncSetAttribute(k_fused_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem), "bwd tc smem"));
-    init = true;
-  }
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
+    return check_cuda(cudaFuncSetAttribute(k_fused_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem), "bwd tc smem");
+  }));
   const unsigned grid = (unsigned)((n + kBzCta - 1) / kBzCta);
   return launch_pdl(k_fused_bwd_tc, dim3(grid), dim3(kBwdThreads), smem, st, "k_fused_bwd_tc", z, m, n,
                     ldz, delta, C, F, col_cos, col_sin, dw, w, lr, l2);

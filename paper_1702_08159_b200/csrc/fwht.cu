@@ -276,15 +276,16 @@ int launch_cluster_t(float* data, int64_t rows, cudaStream_t st) {
   using C = RowCfg<14, 5>;
   const size_t smem = (size_t)C::SMEM_FLOATS * sizeof(float);
   auto kern = fwht_cluster_kernel<K>;
-  static bool init = false;
-  if (!init) {
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
     MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "fwht cluster smem"));
     if (K > 8)
       MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                          "fwht cluster size"));
-    init = true;
-  }
+    return MCK_OK;
+  }));
   for (int64_t r0 = 0; r0 < rows; r0 += (1ll << 26)) {
     const int64_t nr = rows - r0 < (1ll << 26) ? rows - r0 : (1ll << 26);
     cudaLaunchConfig_t cfg{};

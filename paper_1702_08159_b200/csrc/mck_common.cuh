@@ -8,8 +8,10 @@
 // * error state for the C ABI (mck_last_error).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <cuda_runtime.h>
@@ -59,6 +61,43 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.numAttrs = 1;
   MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), what));
   return check_launch(what);
+}
+
+// ---------------------------------------------------------------- per-device setup
+// Kernel attributes (cudaFuncSetAttribute) and occupancy are per device, so a
+// launcher's one-time setup is cached per device index, and the first call on
+// each device runs it under a lock (launchers may be called from several host
+// threads).  `init(dev, slot)` fills the slot and returns an MCK status.
+constexpr int kMaxDevices = 64;
+
+struct DeviceSlot {
+  int occ = 0;   // resident CTAs per SM of the kernel
+  int sms = 0;   // multiprocessor count of the device
+};
+
+struct PerDevice {
+  std::atomic<bool> ready[kMaxDevices] = {};
+  DeviceSlot slot[kMaxDevices];
+  std::mutex mu;
+};
+
+template <class F>
+int per_device(PerDevice& pd, const DeviceSlot** out, F&& init) {
+  int dev = 0;
+  MCK_TRY(check_cuda(cudaGetDevice(&dev), "device"));
+  if (dev < 0 || dev >= kMaxDevices) return fail_value("device index %d out of range", dev);
+  if (!pd.ready[dev].load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(pd.mu);
+    if (!pd.ready[dev].load(std::memory_order_relaxed)) {
+      DeviceSlot s;
+      MCK_TRY(check_cuda(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev), "sms"));
+      MCK_TRY(init(dev, s));
+      pd.slot[dev] = s;
+      pd.ready[dev].store(true, std::memory_order_release);
+    }
+  }
+  *out = &pd.slot[dev];
+  return MCK_OK;
 }
 
 // ---------------------------------------------------------------- hashing

@@ -67,7 +67,16 @@ class GradBucket:
     def hits(self):
         return self.flat[-1:]
 
-    def allreduce(self, group=None) -> None:
+    def allreduce(self, group=None, async_op: bool = False):
+        """Sum the bucket over ranks.  With ``async_op`` the collective is
+        enqueued behind the work already on the current stream and a handle
+        is returned; ``handle.wait()`` orders later work after it."""
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-            dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group)
+            return dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+        return _Done() if async_op else None
+
+
+class _Done:
+    def wait(self):
+        return True

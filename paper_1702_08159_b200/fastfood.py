@@ -238,30 +238,59 @@ def _input(spec: FeatureMapSpec, x, device):
     return t, host
 
 
-def _run(spec, blocks, x, features: bool, normalize: bool, variant: str, out=None, rows=None):
+def _row_index(rows, n_rows: int, device):
+    """Gather index -> contiguous int32 tensor on `device`, every entry in [0, n_rows)."""
+    torch = nat.require_cuda()
+    r = rows if isinstance(rows, torch.Tensor) else torch.from_numpy(np.asarray(rows))
+    if r.dim() != 1:
+        raise ValueError("rows must be a 1-D index array")
+    if r.dtype.is_floating_point or r.dtype == torch.bool:
+        raise ValueError("rows must hold integer indices")
+    if r.numel() and (int(r.min()) < 0 or int(r.max()) >= n_rows):
+        raise ValueError(f"rows must lie in [0, {n_rows})")
+    return r.to(device=device, dtype=torch.int32).contiguous()
+
+
+def _check_out(out, m: int, width: int, device):
+    torch = nat.require_cuda()
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float32:
+        raise ValueError("output buffer must be a float32 tensor")
+    if not out.is_cuda or out.device != device:
+        raise ValueError(f"output buffer must live on {device}")
+    if (out.dim() != 2 or out.shape[0] < m or out.shape[1] < width or out.stride(1) != 1
+            or (m > 1 and out.stride(0) < width)):
+        raise ValueError("output buffer has the wrong shape")
+
+
+def _run(spec, blocks, x, features: bool, normalize: bool, variant: str, out=None, rows=None,
+         trusted_rows=False):
     torch = nat.require_cuda()
     bs = _as_blockset(spec, blocks)
     xt, host = _input(spec, x, bs.device)
+    if rows is not None and not trusted_rows:
+        rows = _row_index(rows, xt.shape[0], bs.device)
     m = xt.shape[0] if rows is None else rows.shape[0]
     width = spec.padded_dim * spec.expansions * (2 if features else 1)
     if out is None:
         out = torch.empty((m, width), dtype=torch.float32, device=bs.device)
-    elif out.shape[0] < m or out.shape[1] < width or out.stride(1) != 1:
-        raise ValueError("output buffer has the wrong shape")
+    else:
+        _check_out(out, m, width, bs.device)
     v = _VARIANTS.get(variant)
     if v is None:
         raise ValueError(f"unknown variant {variant!r}")
-    st = nat.stream_handle(bs.device)
     # size-1 leading dims may carry any stride; rows are d floats apart then
     ldx = xt.stride(0) if xt.shape[0] > 1 else spec.input_dim
-    if features:
-        nat.call("mck_features_f32", nat.ptr(bs.tables), spec.input_dim, spec.expansions,
-                 float(spec.kernel.sigma), nat.ptr(xt), m, ldx, nat.ptr(rows),
-                 1 if normalize else 0, nat.ptr(out), out.stride(0), v, st)
-    else:
-        nat.call("mck_zhat_f32", nat.ptr(bs.tables), spec.input_dim, spec.expansions,
-                 float(spec.kernel.sigma), nat.ptr(xt), m, ldx, nat.ptr(rows),
-                 nat.ptr(out), out.stride(0), v, st)
+    ldo = out.stride(0) if out.shape[0] > 1 else width
+    with torch.cuda.device(bs.device):
+        st = nat.stream_handle(bs.device)
+        if features:
+            nat.call("mck_features_f32", nat.ptr(bs.tables), spec.input_dim, spec.expansions,
+                     float(spec.kernel.sigma), nat.ptr(xt), m, ldx, nat.ptr(rows),
+                     1 if normalize else 0, nat.ptr(out), ldo, v, st)
+        else:
+            nat.call("mck_zhat_f32", nat.ptr(bs.tables), spec.input_dim, spec.expansions,
+                     float(spec.kernel.sigma), nat.ptr(xt), m, ldx, nat.ptr(rows),
+                     nat.ptr(out), ldo, v, st)
     if host:
         return out.cpu().numpy() if not isinstance(x, torch.Tensor) else out.cpu()
     return out
@@ -282,10 +311,17 @@ def feature_map_batch(spec: FeatureMapSpec, blocks, x, normalize: bool = True, *
                       variant: str = "fast", out=None, rows=None):
     """[cos z | sin z] features, shape (m, 2*n*E) (fastfood.py:209-226).
 
-    ``rows`` (int32 CUDA tensor) selects x[rows] as the batch (fused gather);
-    ``out`` lets callers stream into a preallocated (m, >= 2nE) buffer.
+    ``rows`` (integer indices, any dtype/device; range-checked) selects
+    x[rows] as the batch (fused gather); ``out`` lets callers stream into a
+    preallocated float32 (m, >= 2nE) buffer on the blocks' device.
     """
     return _run(spec, blocks, x, True, normalize, variant, out, rows)
+
+
+def _feature_rows_device(spec, blocks, x, rows, out, variant="fast"):
+    """Raw pairs of x[rows] for in-package callers whose ``rows`` is already a
+    valid contiguous int32 index on the device (no host synchronisation)."""
+    return _run(spec, blocks, x, True, False, variant, out, rows, trusted_rows=True)
 
 
 def feature_map(spec: FeatureMapSpec, blocks, x, normalize: bool = True, *, variant: str = "fast"):

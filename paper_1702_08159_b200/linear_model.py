@@ -74,13 +74,13 @@ class SoftmaxModel:
         b = torch.as_tensor(np.asarray(b) if not isinstance(b, torch.Tensor) else b)
         if w.dim() != 2 or tuple(b.shape) != (w.shape[0],):
             raise ValueError("W must be (C, F) and b length C")
+        _check_classes(int(w.shape[0]))
         self.w = w.to(device=dev, dtype=torch.float64).contiguous()
         self.b = b.to(device=dev, dtype=torch.float64).contiguous()
 
     @classmethod
     def zeros(cls, num_classes: int, num_features: int, device=None) -> "SoftmaxModel":
-        if num_classes < 2:
-            raise ValueError("need at least two classes")
+        _check_classes(num_classes)
         return cls(np.zeros((num_classes, num_features)), np.zeros(num_classes), device)
 
     @property
@@ -116,6 +116,17 @@ class RunMetrics:
     def save_csv(self, path) -> None:
         with open(path, "w", encoding="utf-8") as f:
             f.write(self.to_csv())
+
+
+MAX_CLASSES = 16  # head kernels (csrc/classifier.cu kMaxClasses); the reference has no limit
+
+
+def _check_classes(num_classes: int) -> None:
+    if num_classes < 2:
+        raise ValueError("need at least two classes")
+    if num_classes > MAX_CLASSES:
+        raise ValueError(f"num_classes must be in 2..{MAX_CLASSES} (B200 head kernels); "
+                         f"got {num_classes}")
 
 
 def _check_labels(labels, num_classes: int) -> None:
@@ -230,6 +241,7 @@ class Trainer:
             raise ValueError(f"spec input_dim {spec.input_dim} != dataset dim {train_ds.dim}")
         if train_ds.dim != test_ds.dim:
             raise ValueError("train and test dimensions differ")
+        _check_classes(int(train_ds.num_classes))
         self.rank, self.ws = world()
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.spec, self.config, self.variant = spec, config, variant
@@ -262,21 +274,37 @@ class Trainer:
             sel = x.index_select(0, rows.long()) if rows is not None else x[:m]
             self.phi[:m].copy_(sel)
             return self.phi
-        fastfood.feature_map_batch(self.spec, self.blocks, x, normalize=False,
-                                   variant=self.variant, out=self.phi, rows=rows)
+        if rows is None:
+            fastfood.feature_map_batch(self.spec, self.blocks, x, normalize=False,
+                                       variant=self.variant, out=self.phi)
+        else:  # slices of the device epoch shuffles: int32, in range by construction
+            fastfood._feature_rows_device(self.spec, self.blocks, x, rows, self.phi, self.variant)
         return self.phi
 
-    def step(self, epoch: int, s: int) -> None:
+    def _rows(self, epoch: int, s: int):
         cfg = self.config
         start = s * cfg.batch_size
         mg = min(cfg.batch_size, self.n - start)
         lo, hi = shard_range(mg, self.rank, self.ws)
-        rows = self.orders[epoch, start + lo:start + hi]
-        ml = hi - lo
+        return self.orders[epoch, start + lo:start + hi], hi - lo, mg
+
+    def _expand(self, epoch: int, s: int) -> None:
+        """Features of this rank's shard of batch s (fused row gather) into phi."""
+        rows, ml, _ = self._rows(epoch, s)
+        if ml > 0:
+            self.featurize(self.X, rows, ml)
+
+    def _grad(self, epoch: int, s: int):
+        """Forward + gradient of batch s from phi.  One rank: the SGD update is
+        fused into the backward and None is returned.  Several ranks: the
+        partial [dW | db | loss] is written to the bucket and its all-reduce
+        is issued asynchronously; the work handle is returned."""
+        cfg = self.config
+        rows, ml, mg = self._rows(epoch, s)
         st = nat.stream_handle(self.dev)
         loss_ptr = self.step_loss.data_ptr() + 8 * s
+        phi = self.phi
         if ml > 0:
-            phi = self.featurize(self.X, rows, ml)
             self.head.forward(phi, ml, self.model, labels=self.y, label_index=rows, m_total=mg,
                               loss_sum=loss_ptr if self.ws == 1 else self.bucket.loss_sum.data_ptr())
         if self.ws == 1:
@@ -286,7 +314,7 @@ class Trainer:
                      nat.ptr(self.head.delta), self.C, nat.ptr(self.model.w),
                      nat.ptr(self.model.b), float(cfg.learning_rate), float(cfg.l2_lambda),
                      nat.ptr(self.head.scratch), st)
-            return
+            return None
         b = self.bucket
         if ml > 0:
             nat.call("mck_head_backward", nat.ptr(phi), ml, self.F, phi.stride(0),
@@ -294,13 +322,43 @@ class Trainer:
                      nat.ptr(self.head.scratch), st)
         else:
             b.flat.zero_()
-        b.allreduce()
+        return b.allreduce(async_op=True)
+
+    def _update(self, s: int, work) -> None:
+        """Wait for batch s's all-reduce and apply the identical update on every rank."""
+        if self.ws == 1:
+            return
+        cfg = self.config
+        _, _, mg = self._rows(0, s)
+        b = self.bucket
+        work.wait()
         if cfg.l2_lambda:
             b.loss_sum.add_(mg * cfg.l2_lambda * (self.model.w * self.model.w).sum())
         self.step_loss[s:s + 1].copy_(b.loss_sum)
         nat.call("mck_head_sgd_update", nat.ptr(self.model.w), nat.ptr(self.model.b),
                  nat.ptr(b.dw), nat.ptr(b.db), self.F, self.C, float(cfg.learning_rate),
-                 float(cfg.l2_lambda), st)
+                 float(cfg.l2_lambda), nat.stream_handle(self.dev))
+
+    def step(self, epoch: int, s: int) -> None:
+        """One SGD step on global batch s of `epoch` (linear_model.py:213-220)."""
+        self._expand(epoch, s)
+        self._update(s, self._grad(epoch, s))
+
+    def run_epoch(self, epoch: int) -> None:
+        """All steps of an epoch.  With several ranks the expansion of batch
+        s+1 is enqueued while batch s's gradient all-reduce is in flight (it
+        does not depend on W), so the collective overlaps the expansion."""
+        if self.ws == 1:
+            for s in range(self.steps):
+                self.step(epoch, s)
+            return
+        if self.steps:
+            self._expand(epoch, 0)
+        for s in range(self.steps):
+            work = self._grad(epoch, s)
+            if s + 1 < self.steps:
+                self._expand(epoch, s + 1)
+            self._update(s, work)
 
     def batch_sizes(self):
         cfg = self.config
@@ -340,8 +398,7 @@ def train(spec, train_ds, test_ds, config: TrainConfig, *, variant: str = "fast"
     tr = Trainer(spec, train_ds, test_ds, config, variant=variant, eval_chunk=eval_chunk)
     metrics = RunMetrics()
     for epoch in range(config.epochs):
-        for s in range(tr.steps):
-            tr.step(epoch, s)
+        tr.run_epoch(epoch)
         acc, _ = tr.evaluate()
         metrics.records.append(EpochRecord(epoch, tr.epoch_loss(), acc))
     return tr.model, metrics

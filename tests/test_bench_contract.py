@@ -42,3 +42,14 @@ def test_our_arm_fails_without_gpu():
     r = _run("--steps", "1", "--warmup", "3", "--no-extras", timeout=300)
     assert r.returncode != 0
     assert not r.stdout.strip(), "no bench line may be printed without a GPU"
+
+
+def test_gpus_flag_launches_ranks():
+    # `bench.py --gpus 2` outside torchrun starts 2 ranks itself; rank 0 prints the line
+    r = _run("--gpus", "2", "--impl", "reference", "--steps", "1", "--warmup", "0",
+             "--cpu-rows", "16")
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "launching 2 ranks" in r.stderr
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2

@@ -121,6 +121,33 @@ class TestFactors:
             want = {"b": z[f"b{e}"], "perm": z[f"perm{e}"], "g": z[f"g{e}"], "c": z[f"c{e}"]}
             _assert_factors({k: v[e] for k, v in got.items()}, want, f"c4 block {e}")
 
+    def test_config4_all_blocks(self, cuda):
+        """Every one of the 32 c4 blocks (n = 16384): B and Pi bit-exact, G with
+        0 fp32 mismatches against the oracle streams (fastfood.py:145-159), and
+        C-RBF at 6 sampled entries per block (fastfood.py:96-107; the oracle's
+        rbf_c_entries is pinned to the reference at blocks 0/31 by
+        c4_blocks.npz)."""
+        z = load_npz("c4_blocks.npz")
+        meta = json.loads(str(z["meta"][0]))
+        spec = _spec(meta)
+        _, got = _device_blocks(spec)
+        ospec = off.OSpec.of(spec)
+        n, seed = ospec.n, ospec.seed
+        rng = np.random.default_rng(16384)
+        g_mis = c_mis = 0
+        for e in range(spec.expansions):
+            np.testing.assert_array_equal(got["b"][e], od.Stream(seed, "B", e).signs(n).astype(np.float32),
+                                          err_msg=f"c4 block {e} B")
+            np.testing.assert_array_equal(got["perm"][e], od.fisher_yates(od.Stream(seed, "Pi", e), n),
+                                          err_msg=f"c4 block {e} Pi")
+            g = od.Stream(seed, "G", e).gaussians(n).astype(np.float32)
+            g_mis += int((got["g"][e] != g).sum())
+            entries = np.concatenate([[0, n - 1], rng.choice(n, 4, replace=False)])
+            c = off.rbf_c_entries(ospec, e, entries)
+            c_mis += int((got["c"][e][entries] != c).sum())
+        print(f"c4 all blocks: G mismatches {g_mis}/{32 * n}, C mismatches {c_mis}/{32 * 6}")
+        assert g_mis == 0 and c_mis == 0
+
 
 # ---------------------------------------------------------------- transforms
 def _scale_close(got, want, rtol=1e-6):
