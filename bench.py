@@ -425,10 +425,11 @@ def extras(args, P, torch, dev, hbm, rank, ws, cpu):
         fc.step(x4, y4, m_total=mt, lr=0.01)
     ms4 = timed(lambda: fc.step(x4, y4, m_total=mt, lr=0.01), 5, torch, ws, dev)
     n4, E4, rows4 = 16384, 32, 1024
-    # algorithmic lane work per step: two expansions (forward, backward recompute)
-    # of every (row, block): 2 FWHTs x (n/2 log2 n butterflies x 2 add/sub)
-    # + G and C multiplies; MUFU: cos and sin of every z in both passes.
-    lane_ops = 2 * rows4 * E4 * (2 * (n4 // 2) * 14 * 2 + 2 * n4)
+    # algorithmic lane work per step: one expansion of every (row, block):
+    # 2 FWHTs x (n/2 log2 n butterflies x 2 add/sub) + G and C multiplies
+    # (the backward reuses the forward's z); MUFU: cos and sin of every z in
+    # the forward and again in the backward (features are never stored).
+    lane_ops = rows4 * E4 * (2 * (n4 // 2) * 14 * 2 + 2 * n4)
     mufu = 2 * rows4 * E4 * 2 * n4
     f_sm = sm_clock_hz()
     lane_peak = 148 * 128 * f_sm

@@ -160,10 +160,20 @@ int mck_head_backward_sgd(const float* phi, int64_t m, int64_t num_features,
  * mck_fused_scratch_bytes(m, n, C). */
 int64_t mck_fused_scratch_bytes(int64_t m, int64_t n, int32_t num_classes);
 
+/* Scratch for E blocks; keep_z != 0 sizes it for variant bit 2 (z of all E
+ * blocks kept by the forward, m * n * E floats, and reused by the backward
+ * instead of recomputing the expansion). */
+int64_t mck_fused_scratch_bytes_ex(int64_t m, int64_t n, int32_t expansions, int32_t num_classes,
+                                   int32_t keep_z);
+
 /* logits = phi W^T (+ b inside the softmax), softmax, loss_sum, hits and
  * delta = (probs - onehot) / m_total, as mck_head_forward.  delta required.
- * variant 0: contraction on the tensor cores (tcgen05 kind::tf32, 3xTF32 split,
- * TMEM accumulators); variant 1: CUDA-core fp32 FMA (cross-check). */
+ * variant bit 0 clear: contraction on the tensor cores (tcgen05 kind::tf32,
+ * 3xTF32 split, TMEM accumulators); set: CUDA-core fp32 FMA (cross-check).
+ * variant bit 1 (value 2): keep z -- the forward leaves z of all E blocks in
+ * scratch (sized by mck_fused_scratch_bytes_ex(..., keep_z = 1)) and the
+ * following backward / backward_bucket calls on the SAME x, rows and m read
+ * it instead of recomputing the expansion. */
 int mck_fused_forward(const void* tables, int64_t input_dim, int32_t expansions, double sigma,
                       const float* x, int64_t m, int64_t ldx, const int32_t* row_index,
                       const float* w, const double* b, int32_t num_classes,

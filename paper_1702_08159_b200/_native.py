@@ -49,6 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "mck_head_backward_sgd": (C.c_int, [_p, _i64, _i64, _i64, _p, _i32, _p, _p, _f64, _f64, _p,
                                         _p]),
     "mck_fused_scratch_bytes": (_i64, [_i64, _i64, _i32]),
+    "mck_fused_scratch_bytes_ex": (_i64, [_i64, _i64, _i32, _i32, _i32]),
     "mck_fused_forward": (C.c_int, [_p, _i64, _i32, _f64, _p, _i64, _i64, _p, _p, _p, _i32, _p,
                                     _p, _i64, _p, _p, _p, _p, _p, _p, _i32, _p]),
     "mck_fused_backward": (C.c_int, [_p, _i64, _i32, _f64, _p, _i64, _i64, _p, _p, _i32, _p, _p,

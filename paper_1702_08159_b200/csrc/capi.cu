@@ -61,7 +61,7 @@ int head_backward_sgd(const float*, int64_t, int64_t, int64_t, const double*, in
 int head_sgd_update(double*, double*, const double*, const double*, int64_t, int32_t, double,
                     double, cudaStream_t);
 int64_t head_scratch_bytes(int64_t, int64_t, int32_t);
-int64_t fused_scratch_bytes(int64_t, int64_t, int32_t);
+int64_t fused_scratch_bytes(int64_t, int64_t, int32_t, int32_t, bool);
 int fused_forward(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
                   const int32_t*, const float*, const double*, int32_t, const int32_t*,
                   const int32_t*, int64_t, double*, double*, double*, double*, int64_t*, void*,
@@ -282,7 +282,12 @@ extern "C" {
 
 int64_t mck_fused_scratch_bytes(int64_t m, int64_t n, int32_t C) {
   if (m < 0 || n < 1 || C < 2) return 0;
-  return fused_scratch_bytes(m, n, C);
+  return fused_scratch_bytes(m, n, 1, C, false);
+}
+
+int64_t mck_fused_scratch_bytes_ex(int64_t m, int64_t n, int32_t E, int32_t C, int32_t keep_z) {
+  if (m < 0 || n < 1 || E < 1 || C < 2) return 0;
+  return fused_scratch_bytes(m, n, E, C, keep_z != 0);
 }
 
 int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double sigma,
@@ -293,6 +298,7 @@ int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double s
                       int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
+  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
   if (m > 0 && (!w || !b || !delta || !scratch)) return fail_value("NULL argument");
   if (m_total < m) m_total = m;
   TablesView tv;
@@ -308,6 +314,7 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double 
                        double lr, double l2, void* scratch, int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
+  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
   if (m > 0 && (!delta || !scratch)) return fail_value("NULL argument");
   if (w && !(lr > 0.0)) return fail_value("learning rate must be positive");
   if (!w && !dw) return fail_value("either w (fused update) or dw is required");
@@ -325,6 +332,7 @@ int mck_fused_backward_bucket(const void* tables, int64_t input_dim, int32_t E, 
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
   if (e_begin < 0 || e_count < 1 || e_begin + e_count > E)
     return fail_value("block range [%d, %d) outside 0..%d", e_begin, e_begin + e_count, E);
+  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
   if (!bucket || (m > 0 && (!delta || !scratch))) return fail_value("NULL argument");
   if (C < 2 || C > 16) return fail_value("num_classes must be in 2..16");
   if (m == 0)

@@ -992,7 +992,7 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   p.soff = tv.soff; p.ggath = tv.ggath;
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
-  p.keep_l2 = 1;
+  p.keep_l2 = 0;  // the tile (1-2 GiB) is far larger than L2: no eviction hint
   return launch_by_logn(p, logn, false, fold, st);
 }
 

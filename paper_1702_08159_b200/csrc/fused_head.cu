@@ -54,8 +54,12 @@ constexpr int kBz = kBzPerThread * kBthreads;  // z values per backward CTA
 constexpr int kBrowChunk = 128;
 constexpr int kFusedMaxClasses = 16;
 
+// Variant bits of mck_fused_forward/backward.
+constexpr int32_t kVarCudaCores = 1;  // CUDA-core contractions (cross-check)
+constexpr int32_t kVarKeepZ = 2;      // forward keeps z of all E blocks; backward reuses it
+
 struct FusedScratch {
-  float* z;          // [m][kFusedZBlocks * n]
+  float* z;          // [groups][m][kFusedZBlocks n]: all E blocks (kept z) or one group
   float* lpart;      // [KS][m][C]     partial logits of the current block group
   double* logits;    // [m][C]
   double* rowloss;   // [m]
@@ -70,7 +74,19 @@ inline int64_t fused_rsplits(int64_t m) {
   return rs > 16 ? 16 : (rs < 1 ? 1 : rs);
 }
 
-inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedScratch* fs) {
+inline int64_t fused_zgroups(int32_t E, bool keep) {
+  return keep ? (E + kFusedZBlocks - 1) / kFusedZBlocks : 1;
+}
+
+// z of block e: group tile (e / 16) when kept (row stride 16 n, the same
+// layout as the one-group tile of the recompute mode), columns (e % 16) n.
+inline float* fused_zptr(float* z, int64_t m, int64_t n, int32_t e, bool keep) {
+  return keep ? z + (int64_t)(e / kFusedZBlocks) * m * n * kFusedZBlocks + (int64_t)(e % kFusedZBlocks) * n
+              : z;
+}
+
+inline int64_t fused_layout(int64_t m, int64_t n, int32_t E, int32_t C, bool keep, char* base,
+                            FusedScratch* fs) {
   auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   int64_t off = 0;
   auto take = [&](int64_t bytes) {
@@ -82,7 +98,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t C, char* base, FusedSc
   const int64_t KS_cc = (nz + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(nz);
   const int64_t KS = KS_cc > KS_tc ? KS_cc : KS_tc;   // partial-logit chunks of either variant
   FusedScratch s{};
-  s.z = (float*)take(m * n * kFusedZBlocks * 4);
+  s.z = (float*)take(fused_zgroups(E, keep) * m * n * kFusedZBlocks * 4);
   s.lpart = (float*)take(KS * m * C * 4);
   s.logits = (double*)take(m * C * 8);
   s.rowloss = (double*)take(m * 8);
@@ -300,7 +316,9 @@ static int dispatch_nc(int C, Fn fn) {
   }
 }
 
-int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t C) { return fused_layout(m, n, C, nullptr, nullptr); }
+int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t E, int32_t C, bool keep) {
+  return fused_layout(m, n, E, C, keep, nullptr, nullptr);
+}
 
 int fused_fwd_tc(const float*, int64_t, int64_t, int64_t, const float*, int64_t, int, int64_t, int64_t,
                  float*, cudaStream_t);
@@ -312,11 +330,12 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                   int64_t ldx, const int32_t* rows, const float* w, const double* b, int32_t C,
                   const int32_t* labels, const int32_t* label_index, int64_t m_total,
                   double* logits_out, double* probs, double* delta, double* loss_sum,
-                  int64_t* hits, void* scratch, int32_t cuda_cores, cudaStream_t st) {
+                  int64_t* hits, void* scratch, int32_t variant, cudaStream_t st) {
+  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ;
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;
-  fused_layout(m, n, C, (char*)scratch, &fs);
+  fused_layout(m, n, (int32_t)E, C, keep, (char*)scratch, &fs);
   // Blocks e .. e+nb-1 are contiguous in z (tile columns), in W (cos and
   // sin columns) and in the partial-logit chunks: one contraction and one
   // fold per group, over nb*n z values.
@@ -325,13 +344,14 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
     const int32_t nb = (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks);
     const int64_t nz = (int64_t)nb * n;
     const int64_t KS = cuda_cores ? (nz + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(nz);
-    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, fs.z, ldz, st));
+    float* zg = fused_zptr(fs.z, m, n, e, keep);  // this group's z tile
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zg, ldz, st));
     if (!cuda_cores)
-      MCK_TRY(fused_fwd_tc(fs.z, m, nz, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+      MCK_TRY(fused_fwd_tc(zg, m, nz, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
     else MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
-      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(fs.z, m, nz, ldz, w, F, (int64_t)e * n,
+      k_fused_fwd<NC><<<grid, kFwarps * 32, 0, st>>>(zg, m, nz, ldz, w, F, (int64_t)e * n,
                                                      D + (int64_t)e * n, fs.lpart);
       return check_launch("k_fused_fwd");
     }));
@@ -357,31 +377,36 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
                          int64_t ldx, const int32_t* rows, const double* delta, int32_t C,
                          int32_t e_begin, int32_t e_count, float* dw, int64_t ldw, int64_t cos0,
                          int64_t sin0, float* w, double lr, double l2, void* scratch,
-                         int32_t cuda_cores, cudaStream_t st) {
+                         int32_t variant, cudaStream_t st) {
   if (m == 0) return MCK_OK;
+  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ;
   const int64_t n = tv.n;
   FusedScratch fs;
-  fused_layout(m, n, C, (char*)scratch, &fs);
+  fused_layout(m, n, (int32_t)tv.E, C, keep, (char*)scratch, &fs);
   const int64_t RS = fused_rsplits(m);
   const int64_t rps = (m + RS - 1) / RS;
   k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
   MCK_TRY(check_launch("k_to_f32"));
   const int64_t ldz = n * kFusedZBlocks;
   const int32_t e_end = e_begin + e_count;
-  for (int32_t e = e_begin; e < e_end; e += kFusedZBlocks) {
-    const int32_t nb = (int32_t)(e_end - e < kFusedZBlocks ? e_end - e : kFusedZBlocks);
+  for (int32_t e = e_begin, nb = 0; e < e_end; e += nb) {
+    // chunks never cross a 16-block boundary (the forward's z groups)
+    const int32_t room = kFusedZBlocks - e % kFusedZBlocks;
+    nb = e_end - e < room ? e_end - e : room;
     const int64_t nz = (int64_t)nb * n;
     const int64_t cc = cos0 + (int64_t)(e - e_begin) * n, cs = sin0 + (int64_t)(e - e_begin) * n;
-    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, fs.z, ldz, st));
+    // kept z: the forward's tile, read as is; otherwise recompute this group
+    float* zg = fused_zptr(fs.z, m, n, e, keep);
+    if (!keep) MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zg, ldz, st));
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_tc(fs.z, m, nz, ldz, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
+      MCK_TRY(fused_bwd_tc(zg, m, nz, ldz, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
                            st));
       continue;
     }
     MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((nz + kBz - 1) / kBz), (unsigned)RS);
-      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(fs.z, m, nz, ldz, fs.delta32, rps, fs.dwpart);
+      k_fused_bwd<NC><<<grid, kBthreads, 0, st>>>(zg, m, nz, ldz, fs.delta32, rps, fs.dwpart);
       return check_launch("k_fused_bwd");
     }));
     int64_t grid = ((int64_t)C * 2 * nz + 255) / 256;
@@ -396,11 +421,11 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
 int fused_backward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                    int64_t ldx, const int32_t* rows, const double* delta, int32_t C, float* dw,
                    double* db, float* w, double* b, double lr, double l2, void* scratch,
-                   int32_t cuda_cores, cudaStream_t st) {
+                   int32_t variant, cudaStream_t st) {
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, D = n * tv.E, F = 2 * D;
   MCK_TRY(fused_backward_range(tv, d, sigma, x, m, ldx, rows, delta, C, 0, (int32_t)tv.E, dw, F, 0, D,
-                               w, lr, l2, scratch, cuda_cores, st));
+                               w, lr, l2, scratch, variant, st));
   k_fused_db<<<C, 256, 0, st>>>(delta, m, C, db, b, lr);
   return check_launch("k_fused_db");
 }

@@ -32,7 +32,8 @@ class FusedClassifier:
     """Softmax head (W float32 C x 2nE, b float64) over fused Fastfood features."""
 
     def __init__(self, spec, num_classes: int, max_rows: int, device=None, *,
-                 tensor_cores: bool = True, bucket_blocks: int = BUCKET_BLOCKS):
+                 tensor_cores: bool = True, bucket_blocks: int = BUCKET_BLOCKS,
+                 keep_z: bool = True):
         torch = nat.require_cuda()
         _check_classes(num_classes)
         self.dev = torch.device(device) if device is not None else torch.device("cuda")
@@ -45,13 +46,17 @@ class FusedClassifier:
         self.max_rows = max_rows
         self.w = torch.zeros((num_classes, self.F), dtype=torch.float32, device=self.dev)
         self.b = torch.zeros(num_classes, dtype=torch.float64, device=self.dev)
-        nbytes = nat.lib().mck_fused_scratch_bytes(max_rows, spec.padded_dim, num_classes)
+        # keep_z: the forward's z of all blocks (m x nE fp32; 2 GiB at 1,024 c4 rows) stays
+        # in scratch for the backward, which then skips the second expansion
+        nbytes = nat.lib().mck_fused_scratch_bytes_ex(max_rows, spec.padded_dim, spec.expansions,
+                                                      num_classes, 1 if keep_z else 0)
         self.scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         self.delta = torch.empty((max_rows, num_classes), dtype=torch.float64, device=self.dev)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.hits = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.rank, self.ws = world()
-        self.variant = 0 if tensor_cores else 1   # tcgen05 contraction / CUDA-core cross-check
+        # bit 0: CUDA-core cross-check instead of tcgen05; bit 1: keep z for the backward
+        self.variant = (0 if tensor_cores else 1) | (2 if keep_z else 0)
         self.bucket_blocks = max(1, int(bucket_blocks))
         self._buckets = None
 

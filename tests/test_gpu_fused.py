@@ -16,7 +16,7 @@ from paper_1702_08159_b200 import synthetic
 pytestmark = pytest.mark.gpu
 
 
-def _case(cuda, spec, m, seed, tc=True):
+def _case(cuda, spec, m, seed, tc=True, keep_z=True):
     import paper_1702_08159_b200 as P
     from paper_1702_08159_b200.large_scale import FusedClassifier
     torch = cuda
@@ -26,16 +26,17 @@ def _case(cuda, spec, m, seed, tc=True):
     else:
         x = torch.randn((m, spec.input_dim), generator=g, device="cuda")
     y = torch.randint(0, 10, (m,), generator=g, device="cuda", dtype=torch.int32)
-    fc = FusedClassifier(spec, 10, m, tensor_cores=tc)
+    fc = FusedClassifier(spec, 10, m, tensor_cores=tc, keep_z=keep_z)
     fc.w.copy_(torch.randn(fc.w.shape, generator=g, device="cuda") * 0.01)
     fc.b.copy_(torch.randn(10, generator=g, device="cuda", dtype=torch.float64) * 0.1)
     phi = P.feature_map_batch(spec, fc.blocks, x, normalize=False).double()
     return fc, x, y, phi
 
 
+@pytest.mark.parametrize("keep_z", [True, False], ids=["keep_z", "recompute_z"])
 @pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
 @pytest.mark.parametrize("which", ["small", "ragged", "c4"])
-def test_fused_forward_backward(cuda, which, tc):
+def test_fused_forward_backward(cuda, which, tc, keep_z):
     import paper_1702_08159_b200 as P
     torch = cuda
     if which == "small":
@@ -44,7 +45,7 @@ def test_fused_forward_backward(cuda, which, tc):
         spec, m = P.FeatureMapSpec(300, 2, P.RBF(1.0), 8), 37
     else:
         spec, m = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4), 8
-    fc, x, y, phi = _case(cuda, spec, m, 11, tc)
+    fc, x, y, phi = _case(cuda, spec, m, 11, tc, keep_z)
     logits = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     probs = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     fc.forward(x, y, logits=logits, probs=probs)
