@@ -168,8 +168,10 @@ int64_t mck_fused_scratch_bytes_ex(int64_t m, int64_t n, int32_t expansions, int
 
 /* logits = phi W^T (+ b inside the softmax), softmax, loss_sum, hits and
  * delta = (probs - onehot) / m_total, as mck_head_forward.  delta required.
- * variant bit 0 clear: contraction on the tensor cores (tcgen05 kind::tf32,
- * 3xTF32 split, TMEM accumulators); set: CUDA-core fp32 FMA (cross-check).
+ * variant bits 0 and 2 select the contraction engine: neither (default):
+ * packed-FFMA2 CUDA-core kernels (MUFU / HBM bound, fused_cc.cu); bit 2
+ * (value 4): tcgen05 tensor cores (kind::tf32, 3xTF32 split, TMEM
+ * accumulators); bit 0 (value 1): simple CUDA-core FMA kernels (cross-check).
  * variant bit 1 (value 2): keep z -- the forward leaves z of all E blocks in
  * scratch (sized by mck_fused_scratch_bytes_ex(..., keep_z = 1)) and the
  * following backward / backward_bucket calls on the SAME x, rows and m read

@@ -298,7 +298,7 @@ int mck_fused_forward(const void* tables, int64_t input_dim, int32_t E, double s
                       int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
-  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
+  if (variant < 0 || variant > 7 || (variant & 5) == 5) return fail_value("unknown fused variant %d", variant);
   if (m > 0 && (!w || !b || !delta || !scratch)) return fail_value("NULL argument");
   if (m_total < m) m_total = m;
   TablesView tv;
@@ -314,7 +314,7 @@ int mck_fused_backward(const void* tables, int64_t input_dim, int32_t E, double 
                        double lr, double l2, void* scratch, int32_t variant, void* st) {
   const int64_t n = next_pow2(input_dim);
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
-  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
+  if (variant < 0 || variant > 7 || (variant & 5) == 5) return fail_value("unknown fused variant %d", variant);
   if (m > 0 && (!delta || !scratch)) return fail_value("NULL argument");
   if (w && !(lr > 0.0)) return fail_value("learning rate must be positive");
   if (!w && !dw) return fail_value("either w (fused update) or dw is required");
@@ -332,7 +332,7 @@ int mck_fused_backward_bucket(const void* tables, int64_t input_dim, int32_t E, 
   MCK_TRY(ff_common(tables, input_dim, E, sigma, x, m, ldx, 0, 0));
   if (e_begin < 0 || e_count < 1 || e_begin + e_count > E)
     return fail_value("block range [%d, %d) outside 0..%d", e_begin, e_begin + e_count, E);
-  if (variant < 0 || variant > 3) return fail_value("unknown fused variant %d", variant);
+  if (variant < 0 || variant > 7 || (variant & 5) == 5) return fail_value("unknown fused variant %d", variant);
   if (!bucket || (m > 0 && (!delta || !scratch))) return fail_value("NULL argument");
   if (C < 2 || C > 16) return fail_value("num_classes must be in 2..16");
   if (m == 0)

@@ -154,6 +154,7 @@ struct FFParams {
   int64_t D;
   int32_t e0;
   int32_t keep_l2;  // z stores tagged L2 evict_last (fused path: the tile is re-read next)
+  int32_t tile8;    // z written in the ZT8 tile layout (ldo = tile columns), fused path
 };
 
 // Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
@@ -186,15 +187,15 @@ k_fastfood(FFParams p) {
 
   const int64_t groups = (p.m + ROWS - 1) / ROWS;
   // XREG: groups strided over the CTAs, all E blocks per group (x read once).
-  // Otherwise (n = 16384): balanced contiguous ranges of (group, block)
-  // items, so that a launch over several blocks fills every wave.
-  static_assert(XREG || !STAGED, "item ranges assume per-item table reads");
+  // Otherwise (n = 16384): (group, block) items, item = group * E + block,
+  // strided over the CTAs (each CTA 55 or 56 items at config 4, so a launch
+  // over several blocks fills every wave).  At any time the CTAs work on one
+  // contiguous run of items, i.e. neighbouring rows of the same block: the
+  // rows sharing a 128-byte line of a ZT8 z tile are written together.
+  static_assert(XREG || !STAGED, "item loop assumes per-item table reads");
   const int64_t items = groups * p.E;
-  const int64_t it_lo = XREG ? 0 : items * blockIdx.x / gridDim.x;
-  const int64_t it_hi = XREG ? 0 : items * (blockIdx.x + 1) / gridDim.x;
-  const int64_t g_first = XREG ? 0 : it_lo / p.E;
   const int64_t my_groups = XREG ? (groups > blockIdx.x ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0)
-                                 : (it_hi > it_lo ? (it_hi - 1) / p.E - g_first + 1 : 0);
+                                 : (items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int64_t total_it = my_groups * p.E;
 
   auto issue = [&](int64_t it) {  // thread 0 only
@@ -221,11 +222,12 @@ k_fastfood(FFParams p) {
   }
 
   for (int64_t gi = 0; gi < my_groups; ++gi) {
-    const int64_t grp = XREG ? blockIdx.x + gi * gridDim.x : g_first + gi;
+    const int64_t slot = blockIdx.x + gi * gridDim.x;  // group (XREG) or item
+    const int64_t grp = XREG ? slot : slot / p.E;
     const int64_t row = grp * ROWS + gid;
     const bool valid = row < p.m;
-    const int e_lo = XREG ? 0 : (int)(grp == it_lo / p.E ? it_lo % p.E : 0);
-    const int e_hi = XREG ? p.E : (int)(grp == (it_hi - 1) / p.E ? (it_hi - 1) % p.E + 1 : p.E);
+    const int e_lo = XREG ? 0 : (int)(slot % p.E);
+    const int e_hi = XREG ? p.E : e_lo + 1;
     // ---- input row, layout L, zero padded (kept in registers for all E blocks)
     const float* xp = p.x + (valid ? (p.rows ? (int64_t)p.rows[row] : row) : 0) * p.ldx;
     auto load_x = [&](float (&dst)[R]) {
@@ -370,7 +372,9 @@ k_fastfood(FFParams p) {
           }
         } else if (valid) {
           const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
-          if (p.keep_l2) st_hint(reinterpret_cast<float4*>(ob + j * 4 * T), z4, pol);
+          if (p.tile8)
+            *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row, (ob + j * 4 * T) - orow)) = z4;
+          else if (p.keep_l2) st_hint(reinterpret_cast<float4*>(ob + j * 4 * T), z4, pol);
           else *reinterpret_cast<float4*>(ob + j * 4 * T) = z4;
         }
       }
@@ -670,7 +674,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
         } else {
           const float4 a = make_float4(z[0].x, z[1].x, z[2].x, z[3].x);
           const float4 b = make_float4(z[0].y, z[1].y, z[2].y, z[3].y);
-          if (p.keep_l2) {
+          if (p.tile8) {
+            const int64_t col = (ob0 + j * 4 * T) - orow0;
+            if (v0) *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row0, col)) = a;
+            if (v1) *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row0 + 1, col)) = b;
+          } else if (p.keep_l2) {
             if (v0) st_hint(reinterpret_cast<float4*>(ob0 + j * 4 * T), a, pol);
             if (v1) st_hint(reinterpret_cast<float4*>(ob1 + j * 4 * T), b, pol);
           } else {
@@ -976,7 +984,7 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
 // producer half of the fused config-4 path (fused_head.cu).
 int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                       int64_t ldx, const int32_t* rows, int32_t e0, int32_t ecount, float* z,
-                      int64_t ldz, cudaStream_t st) {
+                      int64_t ldz, bool tile8, cudaStream_t st) {
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n;
   const float scale = (float)(1.0 / (sigma * sqrt((double)n)));
@@ -993,6 +1001,7 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
   p.keep_l2 = 0;  // the tile (1-2 GiB) is far larger than L2: no eviction hint
+  p.tile8 = tile8 ? 1 : 0;
   return launch_by_logn(p, logn, false, fold, st);
 }
 

@@ -29,7 +29,7 @@
 namespace mck {
 
 int fastfood_z_blocks(const TablesView&, int32_t, double, const float*, int64_t, int64_t,
-                      const int32_t*, int32_t, int32_t, float*, int64_t, cudaStream_t);
+                      const int32_t*, int32_t, int32_t, float*, int64_t, bool, cudaStream_t);
 int head_softmax_from_logits(const double* logits, int64_t m, int32_t C, const double* b,
                              const int32_t* labels, const int32_t* label_index, int64_t m_total,
                              double* probs, double* delta, double* loss_sum, int64_t* hits,
@@ -45,6 +45,11 @@ constexpr int kFzChunk = 256;     // z values (512 features) per forward CTA
 // 5.02, 8 blocks 4.80, 16 blocks 4.70, 32 blocks 6.07.
 constexpr int kFusedZBlocks = 16;
 int64_t fused_tc_ksplits(int64_t n);  // fused_tc.cu
+int64_t fused_cc_ksplits(int64_t nz);  // fused_cc.cu
+int fused_fwd_cc(const float*, int64_t, int64_t, int64_t, int64_t, const float*, int64_t, int, int64_t,
+                 int64_t, float*, float*, cudaStream_t);
+int fused_bwd_cc(const float*, int64_t, int64_t, int64_t, int64_t, const float*, int, int64_t, int64_t,
+                 int64_t, float*, float*, float, float, cudaStream_t);
 constexpr int kFwarps = 8;
 constexpr int kFrowsPerWarp = 4;
 constexpr int kFrows = kFwarps * kFrowsPerWarp;
@@ -55,8 +60,10 @@ constexpr int kBrowChunk = 128;
 constexpr int kFusedMaxClasses = 16;
 
 // Variant bits of mck_fused_forward/backward.
-constexpr int32_t kVarCudaCores = 1;  // CUDA-core contractions (cross-check)
+constexpr int32_t kVarCudaCores = 1;  // simple CUDA-core contractions (cross-check)
 constexpr int32_t kVarKeepZ = 2;      // forward keeps z of all E blocks; backward reuses it
+constexpr int32_t kVarTc = 4;         // tcgen05 contractions (kind::tf32, 3xTF32)
+// neither bit 0 nor bit 2: packed-FFMA2 contractions (fused_cc.cu), the default
 
 struct FusedScratch {
   float* z;          // [groups][m][kFusedZBlocks n]: all E blocks (kept z) or one group
@@ -67,6 +74,7 @@ struct FusedScratch {
   double* delta64;   // [m][C]
   float* delta32;    // [m][C]
   float* dwpart;     // [RS][C][2 nz]  backward partials of the current block group
+  float* wt;         // [16 n][2][16]   W of the group, transposed (FFMA2 forward)
 };
 
 inline int64_t fused_rsplits(int64_t m) {
@@ -78,11 +86,15 @@ inline int64_t fused_zgroups(int32_t E, bool keep) {
   return keep ? (E + kFusedZBlocks - 1) / kFusedZBlocks : 1;
 }
 
-// z of block e: group tile (e / 16) when kept (row stride 16 n, the same
-// layout as the one-group tile of the recompute mode), columns (e % 16) n.
-inline float* fused_zptr(float* z, int64_t m, int64_t n, int32_t e, bool keep) {
-  return keep ? z + (int64_t)(e / kFusedZBlocks) * m * n * kFusedZBlocks + (int64_t)(e % kFusedZBlocks) * n
-              : z;
+inline int64_t fused_mpad(int64_t m) { return (m + 127) & ~int64_t(127); }
+
+// Group tile holding block e's z and the block's first column in it: tile
+// (e / 16) at column (e % 16) n when kept; the single tile at column 0 when
+// recomputed per chunk.  Tiles hold mpad rows of 16 n columns, row-major
+// (tcgen05 / reference engines) or ZT8 (FFMA2 engine).
+inline float* fused_ztile(float* z, int64_t m, int64_t n, int32_t e, bool keep, int64_t* col0) {
+  *col0 = keep ? (int64_t)(e % kFusedZBlocks) * n : 0;
+  return keep ? z + (int64_t)(e / kFusedZBlocks) * fused_mpad(m) * n * kFusedZBlocks : z;
 }
 
 inline int64_t fused_layout(int64_t m, int64_t n, int32_t E, int32_t C, bool keep, char* base,
@@ -98,7 +110,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t E, int32_t C, bool kee
   const int64_t KS_cc = (nz + kFzChunk - 1) / kFzChunk, KS_tc = fused_tc_ksplits(nz);
   const int64_t KS = KS_cc > KS_tc ? KS_cc : KS_tc;   // partial-logit chunks of either variant
   FusedScratch s{};
-  s.z = (float*)take(fused_zgroups(E, keep) * m * n * kFusedZBlocks * 4);
+  s.z = (float*)take(fused_zgroups(E, keep) * fused_mpad(m) * n * kFusedZBlocks * 4);
   s.lpart = (float*)take(KS * m * C * 4);
   s.logits = (double*)take(m * C * 8);
   s.rowloss = (double*)take(m * 8);
@@ -106,6 +118,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t E, int32_t C, bool kee
   s.delta64 = (double*)take(m * C * 8);
   s.delta32 = (float*)take(m * C * 4);
   s.dwpart = (float*)take(fused_rsplits(m) * C * 2 * nz * 4);
+  s.wt = (float*)take(nz * 2 * 16 * 4);
   if (fs) *fs = s;
   return off;
 }
@@ -320,10 +333,10 @@ int64_t fused_scratch_bytes(int64_t m, int64_t n, int32_t E, int32_t C, bool kee
   return fused_layout(m, n, E, C, keep, nullptr, nullptr);
 }
 
-int fused_fwd_tc(const float*, int64_t, int64_t, int64_t, const float*, int64_t, int, int64_t, int64_t,
-                 float*, cudaStream_t);
-int fused_bwd_tc(const float*, int64_t, int64_t, int64_t, const float*, int, int64_t, int64_t, int64_t,
-                 float*, float*, float, float, cudaStream_t);
+int fused_fwd_tc(const float*, int64_t, int64_t, int64_t, int64_t, const float*, int64_t, int, int64_t,
+                 int64_t, float*, cudaStream_t);
+int fused_bwd_tc(const float*, int64_t, int64_t, int64_t, int64_t, const float*, int, int64_t, int64_t,
+                 int64_t, float*, float*, float, float, cudaStream_t);
 int64_t fused_tc_ksplits(int64_t n);
 
 int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
@@ -331,7 +344,8 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                   const int32_t* labels, const int32_t* label_index, int64_t m_total,
                   double* logits_out, double* probs, double* delta, double* loss_sum,
                   int64_t* hits, void* scratch, int32_t variant, cudaStream_t st) {
-  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ;
+  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ, tc = variant & kVarTc;
+  const bool tile8 = !cuda_cores;  // the FFMA2 and tcgen05 engines read ZT8 tiles
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;
@@ -343,11 +357,17 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
   for (int32_t e = 0; e < E; e += kFusedZBlocks) {
     const int32_t nb = (int32_t)(E - e < kFusedZBlocks ? E - e : kFusedZBlocks);
     const int64_t nz = (int64_t)nb * n;
-    const int64_t KS = cuda_cores ? (nz + kFzChunk - 1) / kFzChunk : fused_tc_ksplits(nz);
-    float* zg = fused_zptr(fs.z, m, n, e, keep);  // this group's z tile
-    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zg, ldz, st));
-    if (!cuda_cores)
-      MCK_TRY(fused_fwd_tc(zg, m, nz, ldz, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+    const int64_t KS = tc ? fused_tc_ksplits(nz)
+                          : cuda_cores ? (nz + kFzChunk - 1) / kFzChunk : fused_cc_ksplits(nz);
+    int64_t col0 = 0;
+    float* const zt = fused_ztile(fs.z, m, n, e, keep, &col0);  // col0 = 0: e is a group start
+    float* const zg = zt + col0;
+    MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zg, ldz, tile8, st));
+    if (tc)
+      MCK_TRY(fused_fwd_tc(zt, m, nz, ldz, col0, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.lpart, st));
+    else if (!cuda_cores)
+      MCK_TRY(fused_fwd_cc(zt, m, nz, ldz, col0, w, F, C, (int64_t)e * n, D + (int64_t)e * n, fs.wt,
+                           fs.lpart, st));
     else MCK_TRY(dispatch_nc(C, [&](auto nc) {
       constexpr int NC = decltype(nc)::value;
       dim3 grid((unsigned)((m + kFrows - 1) / kFrows), (unsigned)KS);
@@ -379,7 +399,8 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
                          int64_t sin0, float* w, double lr, double l2, void* scratch,
                          int32_t variant, cudaStream_t st) {
   if (m == 0) return MCK_OK;
-  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ;
+  const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ, tc = variant & kVarTc;
+  const bool tile8 = !cuda_cores;
   const int64_t n = tv.n;
   FusedScratch fs;
   fused_layout(m, n, (int32_t)tv.E, C, keep, (char*)scratch, &fs);
@@ -396,10 +417,17 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
     const int64_t nz = (int64_t)nb * n;
     const int64_t cc = cos0 + (int64_t)(e - e_begin) * n, cs = sin0 + (int64_t)(e - e_begin) * n;
     // kept z: the forward's tile, read as is; otherwise recompute this group
-    float* zg = fused_zptr(fs.z, m, n, e, keep);
-    if (!keep) MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zg, ldz, st));
+    int64_t col0 = 0;
+    float* const zt = fused_ztile(fs.z, m, n, e, keep, &col0);
+    float* const zg = zt + col0;  // row-major engines
+    if (!keep) MCK_TRY(fastfood_z_blocks(tv, d, sigma, x, m, ldx, rows, e, nb, zt, ldz, tile8, st));
+    if (tc) {
+      MCK_TRY(fused_bwd_tc(zt, m, nz, ldz, col0, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
+                           st));
+      continue;
+    }
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_tc(zg, m, nz, ldz, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
+      MCK_TRY(fused_bwd_cc(zt, m, nz, ldz, col0, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
                            st));
       continue;
     }

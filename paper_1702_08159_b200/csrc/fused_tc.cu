@@ -69,7 +69,7 @@ struct FwdSmem {
 };
 
 __global__ void __launch_bounds__(kFwdThreads, 2)
-k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
+k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz, int64_t zc0,
                const float* __restrict__ w, int64_t F, int C, int64_t col_cos, int64_t col_sin, int rtg,
                float* __restrict__ lpart) {
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -101,11 +101,12 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
   auto issue = [&](int s) {
     if (s < stages) {
       const int64_t r = (rt0 + s / SPR) * kTcM + prow;
-      const float* zp = z + (r < m ? r : m - 1) * ldz + z0;
+      const int64_t rr = r < m ? r : m - 1;
       const int zi = (s % SPR) * kFwdStageZ + 4 * q;
       const int slot = s % kFwdZD;
-      cp_async16(&S.zr[slot][0][t], zp + (zi < nz ? zi : 0));
-      cp_async16(&S.zr[slot][1][t], zp + (zi + 4 < nz ? zi + 4 : 0));
+      // ZT8 tile: lanes = consecutive rows of one [128 rows][8 z] unit (1 KB per warp)
+      cp_async16(&S.zr[slot][0][t], z + zt8_offset(ldz, rr, zc0 + z0 + (zi < nz ? zi : 0)));
+      cp_async16(&S.zr[slot][1][t], z + zt8_offset(ldz, rr, zc0 + z0 + (zi + 4 < nz ? zi + 4 : 0)));
     }
     cp_async_commit();  // one group per stage (possibly empty)
   };
@@ -245,7 +246,7 @@ struct BwdSmem {
 };
 
 __global__ void __launch_bounds__(kBwdThreads, 2)
-k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
+k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz, int64_t zc0,
                const float* __restrict__ delta, int C, int64_t F, int64_t col_cos, int64_t col_sin,
                float* dw, float* w, float lr, float l2) {
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -287,10 +288,12 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
       const int64_t rb = (int64_t)s * kBrowStage;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int ch = lane + 32 * j, row = ch >> 4, zq = ch & 15;
+        // chunk -> (ZT8 unit u = zq / 2, row, half): one instruction covers 16
+        // rows x 32 B of one unit, i.e. 512 contiguous bytes
+        const int ch = lane + 32 * j, row = (ch >> 1) & 31, zq = ((ch >> 6) << 1) | (ch & 1);
         const int64_t r = rb + row < m ? rb + row : m - 1;
         const int64_t zi = z0 + 4 * zq < n ? z0 + 4 * zq : 0;
-        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + r * ldz + zi);
+        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + zt8_offset(ldz, r, zc0 + zi));  // ZT8 tile
       }
       const int64_t c0 = rb * C / 4;  // 16-byte chunk index of the stage's first delta
       for (int j = lane; j < kBrowStage * C / 4; j += 32)
@@ -394,8 +397,8 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz,
   if (warp == 0) umma::tmem_free<kBwdTmemCols>(tm);
 }
 
-int fused_fwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float* w, int64_t F, int C,
-                 int64_t col_cos, int64_t col_sin, float* lpart, cudaStream_t st) {
+int fused_fwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, int64_t zc0, const float* w, int64_t F,
+                 int C, int64_t col_cos, int64_t col_sin, float* lpart, cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
   const size_t smem = sizeof(FwdSmem);
   static PerDevice pd;
@@ -413,10 +416,11 @@ int fused_fwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float*
   if (rtg < 1) rtg = 1;
   dim3 grid((unsigned)((RT + rtg - 1) / rtg), (unsigned)KS);
   return launch_pdl(k_fused_fwd_tc, grid, dim3(kFwdThreads), smem, st, "k_fused_fwd_tc", z, m, n, ldz,
-                    w, F, C, col_cos, col_sin, (int)rtg, lpart);
+                    zc0, w, F, C, col_cos, col_sin, (int)rtg, lpart);
 }
 
-int fused_bwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float* delta, int C, int64_t F,
+int fused_bwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, int64_t zc0, const float* delta, int C,
+                 int64_t F,
                  int64_t col_cos, int64_t col_sin, float* dw, float* w, float lr, float l2,
                  cudaStream_t st) {
   if (C > kTcN) return fail_value("num_classes must be <= %d", kTcN);
@@ -429,7 +433,7 @@ int fused_bwd_tc(const float* z, int64_t m, int64_t n, int64_t ldz, const float*
   }));
   const unsigned grid = (unsigned)((n + kBzCta - 1) / kBzCta);
   return launch_pdl(k_fused_bwd_tc, dim3(grid), dim3(kBwdThreads), smem, st, "k_fused_bwd_tc", z, m, n,
-                    ldz, delta, C, F, col_cos, col_sin, dw, w, lr, l2);
+                    ldz, zc0, delta, C, F, col_cos, col_sin, dw, w, lr, l2);
 }
 
 int64_t fused_tc_ksplits(int64_t n) { return (n + kFzCta - 1) / kFzCta; }

@@ -100,6 +100,16 @@ int per_device(PerDevice& pd, const DeviceSlot** out, F&& init) {
   return MCK_OK;
 }
 
+// ---------------------------------------------------------------- z tiles
+// "ZT8" layout of a fused-path z group tile with `cols` columns (config 4):
+// [row / 128][col / 8][row % 128][col % 8].  128 rows x 8 z values form one
+// contiguous 4 KB unit, so the contractions read whole units (forward) or
+// 256-byte runs of 8 rows (backward) instead of 32-byte pieces of rows 1 MB
+// apart; the tile is allocated for m rounded up to 128 rows.
+__host__ __device__ __forceinline__ int64_t zt8_offset(int64_t cols, int64_t row, int64_t col) {
+  return ((((row >> 7) * (cols >> 3)) + (col >> 3)) << 10) + ((row & 127) << 3) + (col & 7);
+}
+
 // ---------------------------------------------------------------- hashing
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t kFmixC1 = 0xFF51AFD7ED558CCDull;

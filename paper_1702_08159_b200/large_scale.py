@@ -26,13 +26,18 @@ from .distributed import world
 from .linear_model import _check_classes
 
 BUCKET_BLOCKS = 16  # blocks per all-reduce bucket = the backward's z group (csrc/fused_head.cu)
+# Contraction engines: packed-FFMA2 CUDA-core kernels (default: with 10
+# classes the contraction is MUFU- and HBM-bound, csrc/fused_cc.cu), tcgen05
+# tensor cores (kind::tf32, 3xTF32 split, csrc/fused_tc.cu) and a simple
+# CUDA-core cross-check.
+ENGINES = {"ffma2": 0, "tcgen05": 4, "reference": 1}
 
 
 class FusedClassifier:
     """Softmax head (W float32 C x 2nE, b float64) over fused Fastfood features."""
 
     def __init__(self, spec, num_classes: int, max_rows: int, device=None, *,
-                 tensor_cores: bool = True, bucket_blocks: int = BUCKET_BLOCKS,
+                 engine: str = "ffma2", bucket_blocks: int = BUCKET_BLOCKS,
                  keep_z: bool = True):
         torch = nat.require_cuda()
         _check_classes(num_classes)
@@ -55,8 +60,11 @@ class FusedClassifier:
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.hits = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.rank, self.ws = world()
-        # bit 0: CUDA-core cross-check instead of tcgen05; bit 1: keep z for the backward
-        self.variant = (0 if tensor_cores else 1) | (2 if keep_z else 0)
+        # contraction engine (bits 0/2) and keep-z (bit 1) of mck_fused_forward/backward
+        if engine not in ENGINES:
+            raise ValueError(f"engine must be one of {sorted(ENGINES)}")
+        self.engine = engine
+        self.variant = ENGINES[engine] | (2 if keep_z else 0)
         self.bucket_blocks = max(1, int(bucket_blocks))
         self._buckets = None
 

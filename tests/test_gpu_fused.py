@@ -16,7 +16,7 @@ from paper_1702_08159_b200 import synthetic
 pytestmark = pytest.mark.gpu
 
 
-def _case(cuda, spec, m, seed, tc=True, keep_z=True):
+def _case(cuda, spec, m, seed, engine="ffma2", keep_z=True):
     import paper_1702_08159_b200 as P
     from paper_1702_08159_b200.large_scale import FusedClassifier
     torch = cuda
@@ -26,7 +26,7 @@ def _case(cuda, spec, m, seed, tc=True, keep_z=True):
     else:
         x = torch.randn((m, spec.input_dim), generator=g, device="cuda")
     y = torch.randint(0, 10, (m,), generator=g, device="cuda", dtype=torch.int32)
-    fc = FusedClassifier(spec, 10, m, tensor_cores=tc, keep_z=keep_z)
+    fc = FusedClassifier(spec, 10, m, engine=engine, keep_z=keep_z)
     fc.w.copy_(torch.randn(fc.w.shape, generator=g, device="cuda") * 0.01)
     fc.b.copy_(torch.randn(10, generator=g, device="cuda", dtype=torch.float64) * 0.1)
     phi = P.feature_map_batch(spec, fc.blocks, x, normalize=False).double()
@@ -34,9 +34,9 @@ def _case(cuda, spec, m, seed, tc=True, keep_z=True):
 
 
 @pytest.mark.parametrize("keep_z", [True, False], ids=["keep_z", "recompute_z"])
-@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
+@pytest.mark.parametrize("engine", ["ffma2", "tcgen05", "reference"])
 @pytest.mark.parametrize("which", ["small", "ragged", "c4"])
-def test_fused_forward_backward(cuda, which, tc, keep_z):
+def test_fused_forward_backward(cuda, which, engine, keep_z):
     import paper_1702_08159_b200 as P
     torch = cuda
     if which == "small":
@@ -45,7 +45,7 @@ def test_fused_forward_backward(cuda, which, tc, keep_z):
         spec, m = P.FeatureMapSpec(300, 2, P.RBF(1.0), 8), 37
     else:
         spec, m = P.FeatureMapSpec(16384, 32, P.RBF(4.0), 4), 8
-    fc, x, y, phi = _case(cuda, spec, m, 11, tc, keep_z)
+    fc, x, y, phi = _case(cuda, spec, m, 11, engine, keep_z)
     logits = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     probs = torch.empty((m, 10), dtype=torch.float64, device="cuda")
     fc.forward(x, y, logits=logits, probs=probs)
@@ -69,12 +69,12 @@ def test_fused_forward_backward(cuda, which, tc, keep_z):
     assert torch.allclose(db, delta.sum(0), rtol=1e-5, atol=max(1e-8, err))
 
 
-@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
-def test_fused_sgd_update_and_gather(cuda, tc):
+@pytest.mark.parametrize("engine", ["ffma2", "tcgen05", "reference"])
+def test_fused_sgd_update_and_gather(cuda, engine):
     import paper_1702_08159_b200 as P
     torch = cuda
     spec = P.FeatureMapSpec(784, 4, P.RBF(1.0), 3)
-    fc, x, y, phi = _case(cuda, spec, 128, 5, tc)
+    fc, x, y, phi = _case(cuda, spec, 128, 5, engine)
     rows = torch.tensor(list(range(0, 128, 2)), dtype=torch.int32, device="cuda")
     w0, b0 = fc.w.clone(), fc.b.clone()
     fc.forward(x, y, rows=rows, m_total=64)
@@ -90,8 +90,8 @@ def test_fused_sgd_update_and_gather(cuda, tc):
     assert torch.allclose(fc.b, b0 - 0.5 * d.sum(0), rtol=1e-6, atol=1e-9)
 
 
-@pytest.mark.parametrize("tc", [True, False], ids=["tcgen05", "cuda_cores"])
-def test_bucketed_backward_equals_plain(cuda, tc):
+@pytest.mark.parametrize("engine", ["ffma2", "tcgen05", "reference"])
+def test_bucketed_backward_equals_plain(cuda, engine):
     """The multi-rank backward (one all-reduce bucket per block range) writes
     the same float32 dW as the single-rank backward, bit for bit, and the
     bucket update equals the fused update."""
@@ -99,7 +99,7 @@ def test_bucketed_backward_equals_plain(cuda, tc):
     from paper_1702_08159_b200 import _native as nat
     torch = cuda
     spec = P.FeatureMapSpec(1000, 5, P.RBF(1.0), 21)        # n = 1024, ragged last bucket
-    fc, x, y, _ = _case(cuda, spec, 70, 13, tc)
+    fc, x, y, _ = _case(cuda, spec, 70, 13, engine)
     fc.bucket_blocks = 2
     m = fc.forward(x, y)
     dw, db = fc.backward()
