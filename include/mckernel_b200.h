@@ -11,7 +11,10 @@
  *    storage) unless the name says host_; sizes are element counts.
  *  - `stream` is a cudaStream_t passed as void*; every call is
  *    stream-ordered and asynchronous, re-entrant, and keeps no global
- *    mutable device state.
+ *    mutable device state -- except the one-time table builders
+ *    (mck_tables_build / mck_tables_from_factors), which synchronise the
+ *    stream: the conflict-free permutation slots are an edge colouring
+ *    computed on the host between two device phases.
  *  - Return value: MCK_OK, MCK_ERR_VALUE (bad argument; the Python layer
  *    raises ValueError with mck_last_error() text, whose wording follows the
  *    reference's messages) or MCK_ERR_CUDA (RuntimeError).
@@ -73,7 +76,9 @@ int64_t mck_tables_bytes(int64_t n, int32_t expansions);
 
 /* fastfood.py:133-166 build_blocks -- realise every block's factors on the
  * device from the seed, then derive the kernel tables.  `tables` must hold
- * mck_tables_bytes(n, E) bytes; n = next_pow2(input_dim). */
+ * mck_tables_bytes(n, E) bytes; n = next_pow2(input_dim) <= 2^20 (Matern:
+ * <= 16384, its calibration costs t*n^2 gaussians per block).  Synchronous
+ * (host edge-colouring step, see Conventions). */
 int mck_tables_build(void* tables, int64_t input_dim, int32_t expansions,
                      int32_t kernel_kind, double sigma, int32_t t, uint64_t seed,
                      void* stream);

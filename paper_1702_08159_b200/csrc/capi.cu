@@ -150,6 +150,9 @@ int mck_tables_build(void* tables, int64_t input_dim, int32_t E, int32_t kind, d
   if (kind == MCK_KERNEL_MATERN && t < 1) return fail_value("t must be a positive integer");
   if (!tables) return fail_value("tables buffer is NULL");
   const int64_t n = next_pow2(input_dim);
+  if (kind == MCK_KERNEL_MATERN && n > 16384)
+    return fail_value("Matern calibration supports padded_dim <= 16384 (got %lld): it costs t*n^2 "
+                      "gaussians per block", (long long)n);
   TablesView tv;
   tables_layout(n, E, (char*)tables, &tv);
   MCK_TRY(build_factors(tv, seed, kind, t, S(st)));

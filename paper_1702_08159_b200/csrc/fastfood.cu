@@ -938,6 +938,95 @@ int launch_ff_cfg(const FFParams& p, bool feat, bool fold, bool vec, cudaStream_
 }
 
 int launch_by_logn(const FFParams& p, int logn, bool feat, bool fold, cudaStream_t st);
+template <class V> int fwht_fast(V*, int64_t, int64_t, cudaStream_t);
+int fwht_parity(float*, int64_t, int64_t, cudaStream_t);
+
+// ---------------------------------------------------------------- n > 16384
+// padded_dim 2^15 .. 2^20: the row no longer fits one SM's registers and
+// shared memory next to its tables, so each block runs as the reference
+// writes it (fastfood.py:189-197), one pass per step over a chunk of rows in
+// scratch (stream-ordered allocation, <= 256 MiB per buffer):
+//   k_lg_load   v = pad(x) * B                  (exact sign flip)
+//   H           the batched FWHT (cluster / two-phase kernels, K1)
+//   k_lg_gather u = v[:, perm] * G
+//   H
+//   k_lg_epi    z = (u * C) * scale; z or [cos z | sin z] * norm into out
+// Same per-element fp32 operations as the fused kernels; the parity variant
+// uses the reference-order FWHT (bit-exact z).
+__global__ void k_lg_load(const float* __restrict__ x, int64_t ldx, int32_t d,
+                          const int32_t* __restrict__ rows, int64_t r0, int64_t nr, int64_t n,
+                          const float* __restrict__ b, float* __restrict__ v) {
+  const int64_t total = nr * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / n, i = t - r * n;
+    const int64_t row = rows ? (int64_t)rows[r0 + r] : r0 + r;
+    v[t] = i < d ? x[row * ldx + i] * b[i] : 0.f;
+  }
+}
+
+__global__ void k_lg_gather(const float* __restrict__ v, int64_t nr, int64_t n,
+                            const int32_t* __restrict__ perm, const float* __restrict__ g,
+                            float* __restrict__ u) {
+  const int64_t total = nr * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / n, i = t - r * n;
+    u[t] = v[r * n + perm[i]] * g[i];
+  }
+}
+
+__global__ void k_lg_epi(const float* __restrict__ u, int64_t nr, int64_t n, const float* __restrict__ c,
+                         float scale, int feat, float norm, float* __restrict__ out, int64_t ldo,
+                         int64_t col, int64_t D) {
+  const int64_t total = nr * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / n, i = t - r * n;
+    const float z = (u[t] * c[i]) * scale;
+    float* o = out + r * ldo + col + i;
+    if (feat) {
+      float sn, cs;
+      sincos_fast(z, sn, cs);
+      o[0] = cs * norm;
+      o[D] = sn * norm;
+    } else {
+      o[0] = z;
+    }
+  }
+}
+
+static int fastfood_large(const TablesView& tv, int32_t d, const float* x, int64_t m, int64_t ldx,
+                          const int32_t* rows, bool feat, float scale, float norm, float* out,
+                          int64_t ldo, int variant, cudaStream_t st) {
+  const int64_t n = tv.n, D = n * tv.E;
+  const int64_t chunk = (int64_t(1) << 26) / n < m ? (int64_t(1) << 26) / n : m;  // rows per pass
+  float* v = nullptr;
+  MCK_TRY(check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&v), (size_t)2 * chunk * n * 4, st),
+                     "large-n scratch"));
+  float* u = v + chunk * n;
+  int rc = MCK_OK;
+  const unsigned grid = 148 * 8;
+  for (int64_t r0 = 0; r0 < m && rc == MCK_OK; r0 += chunk) {
+    const int64_t nr = m - r0 < chunk ? m - r0 : chunk;
+    for (int32_t e = 0; e < tv.E && rc == MCK_OK; ++e) {
+      const int64_t eo = (int64_t)e * n;
+      k_lg_load<<<grid, 256, 0, st>>>(x, ldx, d, rows, r0, nr, n, tv.b + eo, v);
+      if ((rc = check_launch("k_lg_load")) != MCK_OK) break;
+      rc = variant == MCK_WHT_PARITY ? fwht_parity(v, nr, n, st) : fwht_fast<float>(v, nr, n, st);
+      if (rc != MCK_OK) break;
+      k_lg_gather<<<grid, 256, 0, st>>>(v, nr, n, tv.perm + eo, tv.g + eo, u);
+      if ((rc = check_launch("k_lg_gather")) != MCK_OK) break;
+      rc = variant == MCK_WHT_PARITY ? fwht_parity(u, nr, n, st) : fwht_fast<float>(u, nr, n, st);
+      if (rc != MCK_OK) break;
+      k_lg_epi<<<grid, 256, 0, st>>>(u, nr, n, tv.c + eo, scale, feat ? 1 : 0, norm, out + r0 * ldo, ldo,
+                                     eo, D);
+      rc = check_launch("k_lg_epi");
+    }
+  }
+  const int rf = check_cuda(cudaFreeAsync(v, st), "large-n scratch free");
+  return rc != MCK_OK ? rc : rf;
+}
 
 int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, int64_t m,
                  int64_t ldx, const int32_t* rows, bool feat, bool normalize, float* out,
@@ -953,7 +1042,9 @@ int fastfood_run(const TablesView& tv, int32_t d, double sigma, const float* x, 
   const bool fold = frexpf(scale, &ex) == 0.5f;  // power of two
   int logn = 0;
   while ((int64_t(1) << logn) < n) ++logn;
-  if (variant == MCK_WHT_PARITY || logn < 3 || logn > 14) {
+  if (logn > 14)
+    return fastfood_large(tv, d, x, m, ldx, rows, feat, scale, norm, out, ldo, variant, st);
+  if (variant == MCK_WHT_PARITY || logn < 3) {
     const size_t smem = (size_t)2 * n * sizeof(float);
     if (smem > 200 * 1024) return fail_value("parity expansion supports padded_dim <= 16384");
     if (smem > 48 * 1024)

@@ -505,3 +505,40 @@ class TestHostStreaming:
             torch.cuda.synchronize()
             for o, w in zip(outs, want):
                 assert torch.equal(o, w)
+
+
+# ---------------------------------------------------------------- padded_dim > 16384
+@pytest.mark.parametrize("d,E", [(20000, 2), (70000, 1)])
+def test_large_padded_dim_features(cuda, d, E):
+    """padded_dim 32768 / 131072 (fastfood.py:59-62 accepts any input_dim):
+    factors against the oracle streams (B, Pi bit-exact; G 0 mismatches; C-RBF
+    at sampled entries), normalised features within rtol 1e-5 / atol 1e-6 of
+    the oracle run on the same factors, and the parity variant's z bit-exact
+    against the oracle's BLAS-independent reference-order transform."""
+    import paper_1702_08159_b200 as P
+    torch = cuda
+    spec = P.FeatureMapSpec(d, E, P.RBF(3.0), 99)
+    bs, got = _device_blocks(spec)
+    ospec = off.OSpec.of(spec)
+    n = ospec.n
+    for e in range(E):
+        np.testing.assert_array_equal(got["b"][e], od.Stream(99, "B", e).signs(n).astype(np.float32))
+        np.testing.assert_array_equal(got["perm"][e], od.fisher_yates(od.Stream(99, "Pi", e), n))
+        assert (got["g"][e] != od.Stream(99, "G", e).gaussians(n).astype(np.float32)).sum() == 0
+        ent = np.array([0, 1, n // 2, n - 1])
+        assert np.array_equal(got["c"][e][ent], off.rbf_c_entries(ospec, e, ent))
+    oblocks = [off.OBlock(got["b"][e], got["perm"][e].astype(np.int64), got["g"][e], got["c"][e], e)
+               for e in range(E)]
+    x = np.random.default_rng(5).standard_normal((3, d)).astype(np.float32)
+    feat = P.feature_map_batch(spec, bs, torch.from_numpy(x).cuda()).cpu().numpy()
+    want = off.feature_map_batch(ospec, oblocks, x, wht="sequential")
+    np.testing.assert_allclose(feat, want, rtol=1e-5, atol=1e-6)
+    zp = P.apply_zhat_batch(spec, bs, torch.from_numpy(x).cuda(), variant="parity").cpu().numpy()
+    zo = off.apply_zhat_batch(ospec, oblocks, x, wht="sequential")
+    assert np.array_equal(zp, zo)
+
+
+def test_matern_large_padded_dim_rejected(cuda):
+    import paper_1702_08159_b200 as P
+    with pytest.raises(ValueError, match="Matern calibration supports padded_dim <= 16384"):
+        P.build_blocks(P.FeatureMapSpec(20000, 1, P.RBFMatern(1.0, 2), 1))
