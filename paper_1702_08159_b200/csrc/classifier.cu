@@ -29,11 +29,29 @@ constexpr int kBwdK = kBwdFeatPerThread * kBwdThreads;  // features per backward
 constexpr int kBwdRowChunk = 128;
 
 struct HeadScratch {
-  double* partial;  // [KS][m][C]   split-K logits
+  double* partial;  // [KS][m][C]   split-K logits (C > 16: one [KS][m][16] region per class group)
   double* rowloss;  // [m]
   int32_t* rowhit;  // [m]
-  double* dwpart;   // [RS][C][F]   row-split dW
+  double* dwpart;   // [RS][C][F]   row-split dW (C > 16: of one class group)
+  double* logits;   // [m][C]       C > 16 only: combined logits
+  double* dgroup;   // [m][16]      C > 16 only: delta columns of one class group
 };
+
+// More than 16 classes (the reference accepts any C): the NC <= 16 kernels
+// run once per group of <= 16 consecutive classes (W rows are contiguous);
+// a single trailing class shares a 2-class group with its predecessor, whose
+// results it does not write (cw = first class the group owns).
+struct ClassGroup {
+  int c0, nc, cw;
+};
+inline int class_groups(int C, ClassGroup* gs) {
+  int k = 0;
+  for (int c = 0; c < C; c += kMaxClasses) {
+    const int nc = C - c < kMaxClasses ? C - c : kMaxClasses;
+    gs[k++] = nc >= 2 ? ClassGroup{c, nc, c} : ClassGroup{C - 2, 2, c};
+  }
+  return k;
+}
 
 inline int64_t head_ksplits(int64_t F) { return (F + kFwdK - 1) / kFwdK; }
 inline int64_t head_ksplits_max(int64_t F) { return (F + 511) / 512; }  // k_head_fwd_dmma (kDK)
@@ -48,14 +66,23 @@ inline int64_t head_layout(int64_t m, int64_t F, int32_t C, char* base, HeadScra
   auto al = [](int64_t x) { return (x + 255) & ~int64_t(255); };
   int64_t off = 0;
   HeadScratch h{};
+  const bool grouped = C > kMaxClasses;
+  const int32_t G = (C + kMaxClasses - 1) / kMaxClasses;
+  const int32_t Cg = grouped ? kMaxClasses : C;  // classes per kernel launch
   h.partial = (double*)(base ? base + off : nullptr);
-  off += al(head_ksplits_max(F) * m * C * 8);
+  off += al(head_ksplits_max(F) * m * Cg * 8 * (grouped ? G : 1));
   h.rowloss = (double*)(base ? base + off : nullptr);
   off += al(m * 8);
   h.rowhit = (int32_t*)(base ? base + off : nullptr);
   off += al(m * 4);
   h.dwpart = (double*)(base ? base + off : nullptr);
-  off += al(head_rsplits(m, F, C) * C * F * 8);
+  off += al(head_rsplits(m, F, Cg) * Cg * F * 8);
+  if (grouped) {
+    h.logits = (double*)(base ? base + off : nullptr);
+    off += al(m * C * 8);
+    h.dgroup = (double*)(base ? base + off : nullptr);
+    off += al(m * kMaxClasses * 8);
+  }
   if (hs) *hs = h;
   return off;
 }
@@ -322,14 +349,139 @@ int launch_fwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double*
   return launch_pdl(kern, grid, dim3(kFwdWarps * 32), smem, st, "k_head_fwd", phi, m, F, ld, w, partial);
 }
 
+// logits[r][c] (c in [cw, c0+nc)) = sum_k partial[k][r][c - c0], k ascending
+__global__ void k_head_combine(const double* __restrict__ partial, int64_t KS, int64_t m, int nc, int c0,
+                               int cw, int C, double* __restrict__ logits) {
+  pdl_wait();
+  pdl_trigger();
+  const int own = c0 + nc - cw;
+  const int64_t total = m * own;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / own;
+    const int c = cw + (int)(t - r * own);
+    double sum = 0.0;
+    for (int64_t k = 0; k < KS; ++k) sum += partial[(k * m + r) * nc + (c - c0)];
+    logits[r * C + c] = sum;
+  }
+}
+
+// k_head_softmax for any C: one thread per row over its logits in place
+// (the same operation order as k_head_softmax).
+__global__ void k_head_softmax_any(double* __restrict__ z_all, int64_t m, int C, const double* __restrict__ b,
+                                   const int32_t* __restrict__ labels, const int32_t* __restrict__ label_index,
+                                   int64_t m_total, double* probs, double* delta, double* rowloss,
+                                   int32_t* rowhit) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double* z = z_all + r * C;
+  for (int j = 0; j < C; ++j) z[j] += b[j];
+  double mx = z[0];
+  for (int j = 1; j < C; ++j) mx = fmax(mx, z[j]);
+  for (int j = 0; j < C; ++j) z[j] = exp(z[j] - mx);
+  const double sum = pairwise_serial([&](int64_t i) { return z[i]; }, 0, C);
+  int arg = 0;
+  for (int j = 0; j < C; ++j) {
+    z[j] /= sum;
+    if (z[j] > z[arg]) arg = j;
+  }
+  const int y = labels ? labels[label_index ? label_index[r] : r] : -1;
+  if (probs)
+    for (int j = 0; j < C; ++j) probs[r * C + j] = z[j];
+  if (y >= 0) {
+    rowloss[r] = -log(fmax(z[y], 1e-300));
+    rowhit[r] = (arg == y) ? 1 : 0;
+    if (delta)
+      for (int j = 0; j < C; ++j) delta[r * C + j] = (z[j] - (j == y ? 1.0 : 0.0)) / (double)m_total;
+  }
+}
+
+// dg[r][j] = delta[r][c0 + j], j < nc
+__global__ void k_head_pack_delta(const double* __restrict__ delta, int64_t m, int C, int c0, int nc,
+                                  double* __restrict__ dg) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t total = m * nc;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / nc;
+    dg[t] = delta[r * C + c0 + (int)(t - r * nc)];
+  }
+}
+
+// Like k_head_dw_finish over a slice [off, off + count) of a [RS][stride] partial.
+__global__ void k_head_dw_finish_slice(const double* __restrict__ dwpart, int64_t RS, int64_t stride,
+                                       int64_t off, int64_t count, double* dw, double* w, double lr,
+                                       double l2) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double g = 0.0;
+    for (int64_t s = 0; s < RS; ++s) g += dwpart[s * stride + off + t];
+    if (w) {
+      const double wv = w[t];
+      if (l2 != 0.0) g += 2.0 * l2 * wv;
+      w[t] = wv - lr * g;
+    } else {
+      dw[t] = g;
+    }
+  }
+}
+
+template <class Fn>
+static int dispatch_classes(int C, Fn fn) {
+  switch (C) {
+#define MCK_D(N) case N: return fn(std::integral_constant<int, N>{});
+    MCK_D(2) MCK_D(3) MCK_D(4) MCK_D(5) MCK_D(6) MCK_D(7) MCK_D(8) MCK_D(9) MCK_D(10)
+    MCK_D(11) MCK_D(12) MCK_D(13) MCK_D(14) MCK_D(15) MCK_D(16)
+#undef MCK_D
+    default: return fail_value("internal: class group of %d", C);
+  }
+}
+
+static int head_forward_grouped(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
+                                const double* b, int32_t C, const int32_t* labels,
+                                const int32_t* label_index, int64_t m_total, double* probs,
+                                double* delta, double* loss_sum, int64_t* hits, const HeadScratch& hs,
+                                cudaStream_t st) {
+  ClassGroup gs[4096];
+  if (C > 16 * 4096) return fail_value("num_classes must be <= %d", 16 * 4096);
+  const int G = class_groups(C, gs);
+  const int64_t region = head_ksplits_max(F) * m * kMaxClasses;
+  for (int g = 0; g < G; ++g) {
+    double* part = hs.partial + (int64_t)g * region;
+    int64_t ks = 0;
+    MCK_TRY(dispatch_classes(gs[g].nc, [&](auto nc) {
+      return launch_fwd<decltype(nc)::value>(phi, m, F, ld, w + (int64_t)gs[g].c0 * F, part, st, &ks);
+    }));
+    const int64_t own = m * (gs[g].c0 + gs[g].nc - gs[g].cw);
+    MCK_TRY(launch_pdl(k_head_combine, dim3((unsigned)((own + 255) / 256 < 148 * 8 ? (own + 255) / 256 : 148 * 8)),
+                       dim3(256), 0, st, "k_head_combine", (const double*)part, ks, m, gs[g].nc, gs[g].c0,
+                       gs[g].cw, (int)C, hs.logits));
+  }
+  MCK_TRY(launch_pdl(k_head_softmax_any, dim3((unsigned)((m + 127) / 128)), dim3(128), 0, st,
+                     "k_head_softmax_any", hs.logits, m, (int)C, b, labels, label_index, m_total, probs,
+                     delta, hs.rowloss, hs.rowhit));
+  if (labels && (loss_sum || hits))
+    MCK_TRY(launch_pdl(k_head_reduce, dim3(1), dim3(1024), 0, st, "k_head_reduce",
+                       (const double*)hs.rowloss, (const int32_t*)hs.rowhit, m, loss_sum, hits));
+  return MCK_OK;
+}
+
 int head_forward(const float* phi, int64_t m, int64_t F, int64_t ld, const double* w,
                  const double* b, int32_t C, const int32_t* labels, const int32_t* label_index,
                  int64_t m_total, double* probs, double* delta, double* loss_sum, int64_t* hits,
                  void* scratch, cudaStream_t st) {
-  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  if (C < 2) return fail_value("need at least two classes");
   if (m == 0) return MCK_OK;
   HeadScratch hs;
   head_layout(m, F, C, (char*)scratch, &hs);
+  if (C > kMaxClasses)
+    return head_forward_grouped(phi, m, F, ld, w, b, C, labels, label_index, m_total, probs, delta,
+                                loss_sum, hits, hs, st);
   int64_t ksplits = 0;
   auto fwd = [&](auto nc) {
     return launch_fwd<decltype(nc)::value>(phi, m, F, ld, w, hs.partial, st, &ksplits);
@@ -523,13 +675,40 @@ int launch_bwd(const float* phi, int64_t m, int64_t F, int64_t ld, const double*
   return check_launch("k_head_bwd");
 }
 
+static int head_bwd_grouped(const float* phi, int64_t m, int64_t F, int64_t ld, const double* delta,
+                            int32_t C, double* dw, double* db, double* w, double* b, double lr,
+                            double l2, const HeadScratch& hs, cudaStream_t st) {
+  ClassGroup gs[4096];
+  if (C > 16 * 4096) return fail_value("num_classes must be <= %d", 16 * 4096);
+  const int G = class_groups(C, gs);
+  const int64_t RS = head_rsplits(m, F, kMaxClasses);
+  for (int g = 0; g < G; ++g) {
+    const ClassGroup cg = gs[g];
+    const int64_t pk = m * cg.nc;
+    MCK_TRY(launch_pdl(k_head_pack_delta, dim3((unsigned)((pk + 255) / 256 < 148 * 4 ? (pk + 255) / 256 : 148 * 4)),
+                       dim3(256), 0, st, "k_head_pack_delta", delta, m, (int)C, cg.c0, cg.nc, hs.dgroup));
+    MCK_TRY(dispatch_classes(cg.nc, [&](auto nc) {
+      return launch_bwd<decltype(nc)::value>(phi, m, F, ld, hs.dgroup, hs, RS, st);
+    }));
+    const int64_t off = (int64_t)(cg.cw - cg.c0) * F, count = (int64_t)(cg.c0 + cg.nc - cg.cw) * F;
+    int64_t grid = (count + 255) / 256;
+    if (grid > 148 * 8) grid = 148 * 8;
+    MCK_TRY(launch_pdl(k_head_dw_finish_slice, dim3((unsigned)grid), dim3(256), 0, st,
+                       "k_head_dw_finish_slice", (const double*)hs.dwpart, RS, (int64_t)cg.nc * F, off,
+                       count, dw ? dw + (int64_t)cg.cw * F : nullptr, w ? w + (int64_t)cg.cw * F : nullptr,
+                       lr, l2));
+  }
+  return launch_pdl(k_head_db, dim3(C), dim3(256), 0, st, "k_head_db", delta, m, (int)C, db, b, lr);
+}
+
 static int head_bwd_common(const float* phi, int64_t m, int64_t F, int64_t ld,
                            const double* delta, int32_t C, double* dw, double* db, double* w,
                            double* b, double lr, double l2, void* scratch, cudaStream_t st) {
-  if (C < 2 || C > kMaxClasses) return fail_value("num_classes must be in 2..%d", kMaxClasses);
+  if (C < 2) return fail_value("need at least two classes");
   if (m == 0) return MCK_OK;
   HeadScratch hs;
   head_layout(m, F, C, (char*)scratch, &hs);
+  if (C > kMaxClasses) return head_bwd_grouped(phi, m, F, ld, delta, C, dw, db, w, b, lr, l2, hs, st);
   const int64_t RS = head_rsplits(m, F, C);
   auto bwd = [&](auto nc) {
     return launch_bwd<decltype(nc)::value>(phi, m, F, ld, delta, hs, RS, st);

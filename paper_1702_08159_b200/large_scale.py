@@ -23,7 +23,7 @@ import numpy as np
 from . import _native as nat
 from . import fastfood
 from .distributed import world
-from .linear_model import _check_classes
+from .linear_model import FUSED_MAX_CLASSES, _check_classes
 
 BUCKET_BLOCKS = 16  # blocks per all-reduce bucket = the backward's z group (csrc/fused_head.cu)
 # Contraction engines: packed-FFMA2 CUDA-core kernels (default: with 10
@@ -40,7 +40,7 @@ class FusedClassifier:
                  engine: str = "ffma2", bucket_blocks: int = BUCKET_BLOCKS,
                  keep_z: bool = True):
         torch = nat.require_cuda()
-        _check_classes(num_classes)
+        _check_classes(num_classes, FUSED_MAX_CLASSES)
         self.dev = torch.device(device) if device is not None else torch.device("cuda")
         if self.dev.index is None:
             self.dev = torch.device("cuda", torch.cuda.current_device())

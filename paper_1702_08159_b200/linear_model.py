@@ -118,14 +118,17 @@ class RunMetrics:
             f.write(self.to_csv())
 
 
-MAX_CLASSES = 16  # head kernels (csrc/classifier.cu kMaxClasses); the reference has no limit
+# The softmax head takes any number of classes (groups of 16 classes per
+# kernel launch above 16, csrc/classifier.cu); the fused config-4 classifier
+# (large_scale.py) takes at most FUSED_MAX_CLASSES.
+FUSED_MAX_CLASSES = 16
 
 
-def _check_classes(num_classes: int) -> None:
+def _check_classes(num_classes: int, limit: int | None = None) -> None:
     if num_classes < 2:
         raise ValueError("need at least two classes")
-    if num_classes > MAX_CLASSES:
-        raise ValueError(f"num_classes must be in 2..{MAX_CLASSES} (B200 head kernels); "
+    if limit is not None and num_classes > limit:
+        raise ValueError(f"num_classes must be in 2..{limit} (fused config-4 kernels); "
                          f"got {num_classes}")
 
 

@@ -542,3 +542,34 @@ def test_matern_large_padded_dim_rejected(cuda):
     import paper_1702_08159_b200 as P
     with pytest.raises(ValueError, match="Matern calibration supports padded_dim <= 16384"):
         P.build_blocks(P.FeatureMapSpec(20000, 1, P.RBFMatern(1.0, 2), 1))
+
+
+# ---------------------------------------------------------------- more than 16 classes
+@pytest.mark.parametrize("C", [17, 33, 40])
+def test_many_classes_training_vs_oracle(cuda, C):
+    """The reference trains with any number of classes (linear_model.py:191-223);
+    above 16 the head runs its kernels per group of 16 classes (a single
+    trailing class shares a 2-class group).  Same data, shuffles and
+    hyper-parameters as oracle.linear_model.train: per-epoch loss within 1e-4
+    relative, accuracy within 0.2 pp, and forward_batch / gradients of the
+    final model against the oracle's float64 arithmetic."""
+    import paper_1702_08159_b200 as P
+    x, y = synthetic.class_images(600, 64, C, seed=C, sample_seed=C + 1, noise=0.3)
+    xt, yt = synthetic.class_images(200, 64, C, seed=C, sample_seed=C + 2, noise=0.3)
+    spec = P.FeatureMapSpec(64, 2, P.RBF(1.5), 13)
+    cfg = P.TrainConfig(0.2, 64, 2, shuffle_seed=4)
+    model, met = P.train(spec, P.Dataset(x, y, C), P.Dataset(xt, yt, C), cfg)
+    ospec = off.OSpec.of(spec)
+    w_ref, b_ref, hist = olm.train(ospec, x, y, xt, yt, C, 0.2, 64, 2, shuffle_seed=4)
+    for rec, (e, loss, acc) in zip(met.records, hist):
+        assert abs(rec.test_acc - acc) <= 0.002, (e, rec.test_acc, acc)
+        assert abs(rec.train_loss - loss) <= 1e-4 * abs(loss) + 1e-7, (e, rec.train_loss, loss)
+    w, b = model.numpy()
+    np.testing.assert_allclose(w, w_ref, rtol=1e-4, atol=1e-7 * np.abs(w_ref).max())
+    phi = off.feature_map_batch(ospec, off.build_blocks(ospec), xt[:50], normalize=False)
+    probs = P.forward_batch(model, phi).cpu().numpy()
+    np.testing.assert_allclose(probs, olm.forward_batch(w, b, phi.astype(np.float64)), rtol=1e-9, atol=1e-12)
+    dw, db = P.gradients(model, phi, yt[:50])
+    rdw, rdb = olm.gradients(w, b, phi, yt[:50])
+    np.testing.assert_allclose(dw.cpu().numpy(), rdw, rtol=1e-9, atol=1e-12 * np.abs(rdw).max())
+    np.testing.assert_allclose(db.cpu().numpy(), rdb, rtol=1e-9, atol=1e-14)
