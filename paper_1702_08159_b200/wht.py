@@ -107,13 +107,33 @@ class BenchRecord:
     reps: int
 
 
+def _naive_gpu(torch, v):
+    """The reference's naive oracle (wht.py:67-87) on the GPU: float64 product
+    with sign rows (-1)^popcount(i & j) generated in bounded chunks (the same
+    2^22-entry chunks), O(n^2) work and a fixed memory footprint."""
+    n = v.shape[0]
+    x = v.to(torch.float64)
+    out = torch.empty_like(x)
+    j = torch.arange(n, device=v.device, dtype=torch.int64)
+    rows = max(1, min(n, (1 << 22) // n))
+    for r0 in range(0, n, rows):
+        i = torch.arange(r0, min(r0 + rows, n), device=v.device, dtype=torch.int64)
+        a = i[:, None] & j[None, :]
+        for sh in (16, 8, 4, 2, 1):              # parity of popcount
+            a = a ^ (a >> sh)
+        signs = 1.0 - 2.0 * (a & 1).to(torch.float64)
+        out[r0:r0 + len(i)] = signs @ x
+    return out
+
+
 def bench_wht(sizes, repetitions: int = 5, naive_cutoff: int = 1 << 16, dtype=np.float32):
     """Median device time per single-vector transform (CUDA events), Table-1 style.
 
     ``fast_ms`` times ``mck_fwht_f32`` on one resident vector of each size
     (the reference times ``wht_fast`` on the host, wht.py:183-205).
-    ``naive_ms`` times the O(n^2) product with the dense +-1 matrix on the
-    GPU (float32 matmul) up to ``naive_cutoff``, as the reference's oracle.
+    ``naive_ms`` times the reference's naive oracle (float64 product with
+    chunk-generated sign rows, wht.py:67-87) on the GPU up to
+    ``naive_cutoff`` (2^16 by default, as the reference).
     """
     if repetitions < 3:
         raise ValueError("repetitions must be at least 3")
@@ -140,11 +160,8 @@ def bench_wht(sizes, repetitions: int = 5, naive_cutoff: int = 1 << 16, dtype=np
         wht_fast(proto.clone())                     # warm-up
         fast = med(wht_fast)
         naive = None
-        if size <= naive_cutoff and size <= 1 << 13:
-            h = torch.ones((1, 1), dtype=proto.dtype, device="cuda")
-            while h.shape[0] < size:                # Sylvester: H_2n = [[H, H], [H, -H]]
-                h = torch.cat([torch.cat([h, h], 1), torch.cat([h, -h], 1)], 0)
-            naive = med(lambda b: h @ b)
+        if size <= naive_cutoff:
+            naive = med(lambda b: _naive_gpu(torch, b))
         recs.append(BenchRecord(size, fast, naive, repetitions))
     return recs
 

@@ -185,10 +185,17 @@ def test_kernel_check_bench_wht_and_feature_dump(cuda, tmp_path):
     pairs = [(rng.standard_normal(64) * 0.3, rng.standard_normal(64) * 0.3) for _ in range(100)]
     st = kernel_check(spec, pairs)
     assert st.D == 512 and st.pairs == 100 and st.mean_err <= 0.05      # test_fastfood.py:247-258
-    recs = bench_wht([1024, 4096, 1 << 20], repetitions=3)
+    recs = bench_wht([1024, 4096, 1 << 16, 1 << 20], repetitions=3)
     csv = bench_wht_csv(recs).splitlines()
-    assert csv[0] == "size,impl,median_ms,reps" and len(csv) == 1 + 3 + 2
-    assert all(r.fast_ms > 0 for r in recs) and recs[2].naive_ms is None
+    assert csv[0] == "size,impl,median_ms,reps" and len(csv) == 1 + 4 + 3
+    assert all(r.fast_ms > 0 for r in recs) and recs[3].naive_ms is None
+    assert recs[2].naive_ms is not None                      # naive oracle up to 2^16 (wht.py:187)
+    import torch
+    from paper_1702_08159_b200.wht import _naive_gpu, wht_fast
+    v = torch.randn(4096, device="cuda", dtype=torch.float32)
+    nv = _naive_gpu(torch, v)
+    fv = wht_fast(v.clone()).double()
+    assert (nv - fv).abs().max().item() <= 1e-6 * nv.abs().max().item()
     x = synthetic.image_rows(300, 784, 3)
     spec2 = P.FeatureMapSpec(784, 2, P.RBF(1.0), 9)
     bs = P.build_blocks(spec2)
