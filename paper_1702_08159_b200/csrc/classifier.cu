@@ -55,9 +55,12 @@ inline int class_groups(int C, ClassGroup* gs) {
 
 inline int64_t head_ksplits(int64_t F) { return (F + kFwdK - 1) / kFwdK; }
 inline int64_t head_ksplits_max(int64_t F) { return (F + 511) / 512; }  // k_head_fwd_dmma (kDK)
+#ifndef MCK_HEAD_RS_MAX
+#define MCK_HEAD_RS_MAX 8
+#endif
 inline int64_t head_rsplits(int64_t m, int64_t F, int32_t C) {
   int64_t rs = (int64_t(1) << 22) / ((int64_t)C * F);  // keep dW partials <= 32 MB
-  if (rs > 16) rs = 16;
+  if (rs > MCK_HEAD_RS_MAX) rs = MCK_HEAD_RS_MAX;
   if (rs > (m + 63) / 64) rs = (m + 63) / 64;
   return rs < 1 ? 1 : rs;
 }
@@ -250,7 +253,10 @@ __global__ void __launch_bounds__(256) k_head_fwd_dmma(const float* __restrict__
 // One CTA per kSmRows rows: thread (row, class) sums the split-K partials of
 // its logit in ascending split order (loads of all splits in flight), then one
 // thread per row finishes the softmax from shared memory.
-constexpr int kSmRows = 32;
+#ifndef MCK_SM_ROWS
+#define MCK_SM_ROWS 4
+#endif
+constexpr int kSmRows = MCK_SM_ROWS;
 __global__ void __launch_bounds__(kSmRows * kMaxClasses)
 k_head_softmax(const double* __restrict__ partial, int64_t KS, int64_t m, int C,
                const double* __restrict__ b, const int32_t* __restrict__ labels,

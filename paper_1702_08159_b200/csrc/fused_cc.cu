@@ -97,13 +97,15 @@ __global__ void k_fused_wt(const float* __restrict__ w, int64_t F, int C, int NC
                            int64_t col_sin, int64_t nz, float* __restrict__ wt) {
   pdl_wait();
   pdl_trigger();
-  const int64_t total = nz * 2 * NCP;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / (2 * NCP);
-    const int k = (int)(t - i * 2 * NCP);
-    const int c = k < NCP ? k : k - NCP;
-    wt[t] = c < C ? w[(int64_t)c * F + (k < NCP ? col_cos : col_sin) + i] : 0.f;
+  // thread per z index: the reads of each class row are coalesced across the
+  // warp, the thread's 2*NCP outputs are contiguous
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float* o = wt + i * 2 * NCP;
+    for (int c = 0; c < NCP; ++c) {
+      o[c] = c < C ? w[(int64_t)c * F + col_cos + i] : 0.f;
+      o[NCP + c] = c < C ? w[(int64_t)c * F + col_sin + i] : 0.f;
+    }
   }
 }
 
