@@ -72,12 +72,6 @@ __device__ __forceinline__ void cp_async16_zfill(void* dst, const void* src, boo
                : "memory");
 }
 
-__device__ __forceinline__ void cp_async4_zfill(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 4 : 0)
-               : "memory");
-}
-
 template <int NCP>
 struct FwdStage {
   float z[kFRows * kFZ];        // row r: 8 z, two 16-byte halves swapped when (r >> 2) & 1
@@ -214,6 +208,8 @@ k_fused_fwd_cc(const float* __restrict__ z, int64_t m, int64_t nz, int64_t zcols
 }
 
 // dW of columns i in [0, nz): g[c][i] = sum_r delta[r][c] cos(z[r][i]) (cos
+// half) / sin (sin half); delta is the zero-padded float32 [rows8][NCP] copy.
+// (cos
 // half) / sin (sin half); written to dw[c*ldw + cos0 + i] / [c*ldw + sin0 + i]
 // or applied as w -= lr*(g + 2*l2*w) at the same positions.
 template <int NCP>
@@ -224,9 +220,6 @@ k_fused_bwd_cc(const float* __restrict__ z, int64_t m, int64_t nz, int64_t zcols
   extern __shared__ __align__(16) unsigned char smraw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   BwdStage<NCP>* ring = reinterpret_cast<BwdStage<NCP>*>(smraw) + warp * kBStages;
-  for (int s = 0; s < kBStages; ++s)  // classes C..NCP-1 stay zero
-    for (int t = lane; t < kBRows * NCP; t += 32) ring[s].d[t] = 0.f;
-  __syncwarp();
   const int64_t items = (nz + kBCols - 1) / kBCols;
   const int64_t nwarps = (int64_t)gridDim.x * kBWarps;
   const int nst = (int)((m + kBRows - 1) / kBRows);
@@ -247,11 +240,8 @@ k_fused_bwd_cc(const float* __restrict__ z, int64_t m, int64_t nz, int64_t zcols
 #pragma unroll
         for (int rr = 0; rr < kBRows; ++rr)
           if (live) cp_async16_zfill(&st.z[rr * kBCols + 4 * lane], unit + rr * 8, rb + rr < m);
-        for (int t = lane; t < kBRows * C; t += 32) {
-          const int rr = t / C, c = t - rr * C;
-          const bool ok = rb + rr < m;
-          cp_async4_zfill(&st.d[rr * NCP + c], delta + (ok ? (rb + rr) * C + c : 0), ok);
-        }
+        // delta: 8 padded rows of NCP floats, contiguous (zero beyond m and C)
+        if (lane < kBRows * NCP / 4) cp_async16(&st.d[4 * lane], delta + rb * NCP + 4 * lane);
       }
       cp_async_commit();
     };

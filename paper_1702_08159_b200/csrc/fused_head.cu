@@ -73,6 +73,7 @@ struct FusedScratch {
   int32_t* rowhit;   // [m]
   double* delta64;   // [m][C]
   float* delta32;    // [m][C]
+  float* delta32p;   // [m rounded up to 8][16]  zero padded (FFMA2 backward)
   float* dwpart;     // [RS][C][2 nz]  backward partials of the current block group
   float* wt;         // [16 n][2][16]   W of the group, transposed (FFMA2 forward)
 };
@@ -117,6 +118,7 @@ inline int64_t fused_layout(int64_t m, int64_t n, int32_t E, int32_t C, bool kee
   s.rowhit = (int32_t*)take(m * 4);
   s.delta64 = (double*)take(m * C * 8);
   s.delta32 = (float*)take(m * C * 4);
+  s.delta32p = (float*)take(((m + 7) & ~int64_t(7)) * 16 * 4);
   s.dwpart = (float*)take(fused_rsplits(m) * C * 2 * nz * 4);
   s.wt = (float*)take(nz * 2 * 16 * 4);
   if (fs) *fs = s;
@@ -216,6 +218,15 @@ k_fused_fold(const float* __restrict__ lpart, int64_t KS, int64_t m, int C, doub
     for (int i = 0; i < kFoldWarps; ++i) r += part[i][lane];
     logits[t] = r;
   }
+}
+
+// padded float32 copy of delta: out[r][c] for r < rows (multiple of 8), c < ncp
+__global__ void k_to_f32_pad(const double* a, int64_t m, int C, int ncp, int64_t rows, float* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * ncp) return;
+  const int64_t r = t / ncp;
+  const int c = (int)(t - r * ncp);
+  out[t] = (r < m && c < C) ? (float)a[r * C + c] : 0.f;
 }
 
 __global__ void k_to_f32(const double* a, float* b, int64_t n) {
@@ -408,6 +419,13 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
   const int64_t rps = (m + RS - 1) / RS;
   k_to_f32<<<(unsigned)((m * C + 255) / 256), 256, 0, st>>>(delta, fs.delta32, m * C);
   MCK_TRY(check_launch("k_to_f32"));
+  if (!tc && !cuda_cores) {
+    const int ncp = (C + 1) & ~1;
+    const int64_t rows8 = (m + 7) & ~int64_t(7);
+    k_to_f32_pad<<<(unsigned)((rows8 * ncp + 255) / 256), 256, 0, st>>>(delta, m, C, ncp, rows8,
+                                                                       fs.delta32p);
+    MCK_TRY(check_launch("k_to_f32_pad"));
+  }
   const int64_t ldz = n * kFusedZBlocks;
   const int32_t e_end = e_begin + e_count;
   for (int32_t e = e_begin, nb = 0; e < e_end; e += nb) {
@@ -427,7 +445,7 @@ int fused_backward_range(const TablesView& tv, int32_t d, double sigma, const fl
       continue;
     }
     if (!cuda_cores) {
-      MCK_TRY(fused_bwd_cc(zt, m, nz, ldz, col0, fs.delta32, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
+      MCK_TRY(fused_bwd_cc(zt, m, nz, ldz, col0, fs.delta32p, C, ldw, cc, cs, dw, w, (float)lr, (float)l2,
                            st));
       continue;
     }
