@@ -154,7 +154,7 @@ struct FFParams {
   int64_t D;
   int32_t e0;
   int32_t keep_l2;  // z stores tagged L2 evict_last (fused path: the tile is re-read next)
-  int32_t tile8;    // z written in the ZT8 tile layout (ldo = tile columns), fused path
+  int32_t tile8;    // z written in the tiled layout (zt_offset, ldo = tile columns), fused path
 };
 
 // Persistent: each CTA walks row groups g = blockIdx.x, +gridDim.x, ...; the
@@ -191,7 +191,7 @@ k_fastfood(FFParams p) {
   // strided over the CTAs (each CTA 55 or 56 items at config 4, so a launch
   // over several blocks fills every wave).  At any time the CTAs work on one
   // contiguous run of items, i.e. neighbouring rows of the same block: the
-  // rows sharing a 128-byte line of a ZT8 z tile are written together.
+  // z tile lines of neighbouring rows are written close together.
   static_assert(XREG || !STAGED, "item loop assumes per-item table reads");
   const int64_t items = groups * p.E;
   const int64_t my_groups = XREG ? (groups > blockIdx.x ? (groups - 1 - blockIdx.x) / gridDim.x + 1 : 0)
@@ -373,7 +373,7 @@ k_fastfood(FFParams p) {
         } else if (valid) {
           const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
           if (p.tile8)
-            *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row, (ob + j * 4 * T) - orow)) = z4;
+            *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row, (ob + j * 4 * T) - orow)) = z4;
           else if (p.keep_l2) st_hint(reinterpret_cast<float4*>(ob + j * 4 * T), z4, pol);
           else *reinterpret_cast<float4*>(ob + j * 4 * T) = z4;
         }
@@ -676,8 +676,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
           const float4 b = make_float4(z[0].y, z[1].y, z[2].y, z[3].y);
           if (p.tile8) {
             const int64_t col = (ob0 + j * 4 * T) - orow0;
-            if (v0) *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row0, col)) = a;
-            if (v1) *reinterpret_cast<float4*>(p.out + zt8_offset(p.ldo, row0 + 1, col)) = b;
+            if (v0) *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row0, col)) = a;
+            if (v1) *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row0 + 1, col)) = b;
           } else if (p.keep_l2) {
             if (v0) st_hint(reinterpret_cast<float4*>(ob0 + j * 4 * T), a, pol);
             if (v1) st_hint(reinterpret_cast<float4*>(ob1 + j * 4 * T), b, pol);

@@ -11,7 +11,7 @@
 // warp works on its own items with its own cp.async ring (no CTA barriers):
 //
 // * forward  (k_fused_fwd_cc): item = 128 rows x kZW z values.  Lane l holds
-//   rows l, l+32, l+64, l+96; a stage brings one ZT8 unit [128 rows][8 z]
+//   rows l, l+32, l+64, l+96; a stage brings a [128 rows][8 z] slice of a z-tile unit
 //   (4 KB contiguous; rows XOR-swizzled in shared memory so the per-row
 //   16-byte reads are conflict free) and
 //   the 8 z values' W (transposed per group to [z][cos classes | sin classes],
@@ -20,7 +20,7 @@
 //   float64 by k_fused_fold (fixed order).
 // * backward (k_fused_bwd_cc): item = 128 z columns x all rows.  Lane l holds
 //   columns 4l..4l+3; a stage brings [8 rows][128 z] of z (16 runs of 256 B
-//   from 16 ZT8 units) and the 8 rows' delta (float32).  dW of the 128 columns is complete at the end of the
+//   of whole 128-byte lines) and the 8 rows' delta (float32).  dW of the 128 columns is complete at the end of the
 //   item: written (plain or all-reduce bucket layout) or applied as the SGD
 //   update in place -- no partial buffers, no second pass.
 //
@@ -86,20 +86,29 @@ struct BwdStage {
 
 }  // namespace
 
-// wt[i][c] = W[c][col_cos + i], wt[i][NCP + c] = W[c][col_sin + i] (0 for c >= C)
-__global__ void k_fused_wt(const float* __restrict__ w, int64_t F, int C, int NCP, int64_t col_cos,
-                           int64_t col_sin, int64_t nz, float* __restrict__ wt) {
+// wt[i][c] = W[c][col_cos + i], wt[i][NCP + c] = W[c][col_sin + i] (0 for c >= C).
+// A CTA transposes 256 z indices through shared memory: coalesced reads of
+// each class row, then the [256][2*NCP] block written linearly.
+__global__ void __launch_bounds__(256) k_fused_wt(const float* __restrict__ w, int64_t F, int C, int NCP,
+                                                  int64_t col_cos, int64_t col_sin, int64_t nz,
+                                                  float* __restrict__ wt) {
+  __shared__ float tile[256 * 33];
   pdl_wait();
   pdl_trigger();
-  // thread per z index: the reads of each class row are coalesced across the
-  // warp, the thread's 2*NCP outputs are contiguous
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float* o = wt + i * 2 * NCP;
-    for (int c = 0; c < NCP; ++c) {
-      o[c] = c < C ? w[(int64_t)c * F + col_cos + i] : 0.f;
-      o[NCP + c] = c < C ? w[(int64_t)c * F + col_sin + i] : 0.f;
+  const int t = threadIdx.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * 256; i0 < nz; i0 += (int64_t)gridDim.x * 256) {
+    const int ni = nz - i0 < 256 ? (int)(nz - i0) : 256;
+    for (int k = 0; k < 2 * NCP; ++k) {
+      const int c = k < NCP ? k : k - NCP;
+      tile[t * 33 + k] = (c < C && t < ni) ? w[(int64_t)c * F + (k < NCP ? col_cos : col_sin) + i0 + t] : 0.f;
     }
+    __syncthreads();
+    const int total = ni * 2 * NCP;
+    for (int e = t; e < total; e += 256) {
+      const int i = e / (2 * NCP), k = e - i * (2 * NCP);
+      wt[i0 * 2 * NCP + e] = tile[i * 33 + k];
+    }
+    __syncthreads();
   }
 }
 
@@ -124,12 +133,13 @@ k_fused_fwd_cc(const float* __restrict__ z, int64_t m, int64_t nz, int64_t zcols
       if (s < nst) {
         FwdStage<NCP>& st = ring[s % kCcStages];
         const int64_t c0 = zb + (int64_t)s * kFZ;
-        // one contiguous ZT8 unit: [128 rows][8 z] (rows >= m are never output)
-        const float* unit = z + zt8_offset(zcols, r0, col0 + c0);
+        // [128 rows][8 z] of the z tile (one contiguous unit when MCK_ZT_LOG == 3;
+        // rows >= m are never output)
+        const float* unit = z + zt_offset(zcols, r0, col0 + c0);
 #pragma unroll
         for (int t = 0; t < (kFRows * 2) / 32; ++t) {
           const int idx = lane + 32 * t, r = idx >> 1, j = idx & 1;
-          cp_async16(&st.z[r * kFZ + ((j ^ ((r >> 2) & 1)) << 2)], unit + idx * 4);
+          cp_async16(&st.z[r * kFZ + ((j ^ ((r >> 2) & 1)) << 2)], unit + (r << MCK_ZT_LOG) + 4 * j);
         }
         for (int idx = lane; idx < kFZ * 2 * NCP / 4; idx += 32)
           cp_async16(&st.w[idx * 4], wt + c0 * 2 * NCP + idx * 4);
@@ -233,13 +243,13 @@ k_fused_bwd_cc(const float* __restrict__ z, int64_t m, int64_t nz, int64_t zcols
       if (s < nst) {
         BwdStage<NCP>& st = ring[s % kBStages];
         const int64_t rb = (int64_t)s * kBRows;
-        // lane: half (lane & 1) of the ZT8 unit of columns col + (0..7); 8 rows of a
-        // unit are one 256-byte run.  Rows >= m are zero-filled (delta is zero
-        // there too, and the tile's padding rows are never written).
-        const float* unit = z + zt8_offset(zcols, rb, col0 + c0 + 8 * (lane >> 1)) + 4 * (lane & 1);
+        // lane: 4 columns of a tile row piece (8 lanes = one 128-byte line).
+        // Rows >= m are zero-filled (delta is zero there too, and the tile's
+        // padding rows are never written).
+        const float* unit = z + zt_offset(zcols, rb, col0 + c0 + 4 * lane);
 #pragma unroll
         for (int rr = 0; rr < kBRows; ++rr)
-          if (live) cp_async16_zfill(&st.z[rr * kBCols + 4 * lane], unit + rr * 8, rb + rr < m);
+          if (live) cp_async16_zfill(&st.z[rr * kBCols + 4 * lane], unit + (rr << MCK_ZT_LOG), rb + rr < m);
         // delta: 8 padded rows of NCP floats, contiguous (zero beyond m and C)
         if (lane < kBRows * NCP / 4) cp_async16(&st.d[4 * lane], delta + rb * NCP + 4 * lane);
       }

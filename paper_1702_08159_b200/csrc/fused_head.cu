@@ -92,7 +92,7 @@ inline int64_t fused_mpad(int64_t m) { return (m + 127) & ~int64_t(127); }
 // Group tile holding block e's z and the block's first column in it: tile
 // (e / 16) at column (e % 16) n when kept; the single tile at column 0 when
 // recomputed per chunk.  Tiles hold mpad rows of 16 n columns, row-major
-// (tcgen05 / reference engines) or ZT8 (FFMA2 engine).
+// (reference engine) or tiled (zt_offset: FFMA2 and tcgen05 engines).
 inline float* fused_ztile(float* z, int64_t m, int64_t n, int32_t e, bool keep, int64_t* col0) {
   *col0 = keep ? (int64_t)(e % kFusedZBlocks) * n : 0;
   return keep ? z + (int64_t)(e / kFusedZBlocks) * fused_mpad(m) * n * kFusedZBlocks : z;
@@ -356,7 +356,7 @@ int fused_forward(const TablesView& tv, int32_t d, double sigma, const float* x,
                   double* logits_out, double* probs, double* delta, double* loss_sum,
                   int64_t* hits, void* scratch, int32_t variant, cudaStream_t st) {
   const bool cuda_cores = variant & kVarCudaCores, keep = variant & kVarKeepZ, tc = variant & kVarTc;
-  const bool tile8 = !cuda_cores;  // the FFMA2 and tcgen05 engines read ZT8 tiles
+  const bool tile8 = !cuda_cores;  // the FFMA2 and tcgen05 engines read tiled z
   if (m == 0) return MCK_OK;
   const int64_t n = tv.n, E = tv.E, D = n * E, F = 2 * D;
   FusedScratch fs;

@@ -104,9 +104,9 @@ k_fused_fwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz, i
       const int64_t rr = r < m ? r : m - 1;
       const int zi = (s % SPR) * kFwdStageZ + 4 * q;
       const int slot = s % kFwdZD;
-      // ZT8 tile: lanes = consecutive rows of one [128 rows][8 z] unit (1 KB per warp)
-      cp_async16(&S.zr[slot][0][t], z + zt8_offset(ldz, rr, zc0 + z0 + (zi < nz ? zi : 0)));
-      cp_async16(&S.zr[slot][1][t], z + zt8_offset(ldz, rr, zc0 + z0 + (zi + 4 < nz ? zi + 4 : 0)));
+      // tiled z: lanes = consecutive rows of one unit
+      cp_async16(&S.zr[slot][0][t], z + zt_offset(ldz, rr, zc0 + z0 + (zi < nz ? zi : 0)));
+      cp_async16(&S.zr[slot][1][t], z + zt_offset(ldz, rr, zc0 + z0 + (zi + 4 < nz ? zi + 4 : 0)));
     }
     cp_async_commit();  // one group per stage (possibly empty)
   };
@@ -288,12 +288,12 @@ k_fused_bwd_tc(const float* __restrict__ z, int64_t m, int64_t n, int64_t ldz, i
       const int64_t rb = (int64_t)s * kBrowStage;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        // chunk -> (ZT8 unit u = zq / 2, row, half): one instruction covers 16
+        // chunk -> (column quad zq, row): one instruction covers 16
         // rows x 32 B of one unit, i.e. 512 contiguous bytes
         const int ch = lane + 32 * j, row = (ch >> 1) & 31, zq = ((ch >> 6) << 1) | (ch & 1);
         const int64_t r = rb + row < m ? rb + row : m - 1;
         const int64_t zi = z0 + 4 * zq < n ? z0 + 4 * zq : 0;
-        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + zt8_offset(ldz, r, zc0 + zi));  // ZT8 tile
+        cp_async16(&S.zr[zb][row * kBzCta + 4 * zq], z + zt_offset(ldz, r, zc0 + zi));  // tiled z
       }
       const int64_t c0 = rb * C / 4;  // 16-byte chunk index of the stage's first delta
       for (int j = lane; j < kBrowStage * C / 4; j += 32)

@@ -101,13 +101,21 @@ int per_device(PerDevice& pd, const DeviceSlot** out, F&& init) {
 }
 
 // ---------------------------------------------------------------- z tiles
-// "ZT8" layout of a fused-path z group tile with `cols` columns (config 4):
-// [row / 128][col / 8][row % 128][col % 8].  128 rows x 8 z values form one
-// contiguous 4 KB unit, so the contractions read whole units (forward) or
-// 256-byte runs of 8 rows (backward) instead of 32-byte pieces of rows 1 MB
-// apart; the tile is allocated for m rounded up to 128 rows.
-__host__ __device__ __forceinline__ int64_t zt8_offset(int64_t cols, int64_t row, int64_t col) {
-  return ((((row >> 7) * (cols >> 3)) + (col >> 3)) << 10) + ((row & 127) << 3) + (col & 7);
+// Tiled layout of a fused-path z group tile with `cols` columns (config 4):
+// [row / 128][col / 2^L][row % 128][col % 2^L], L = MCK_ZT_LOG = 5: each
+// row piece is one 128-byte line and 128 rows x 32 z form a contiguous 16 KB
+// unit.  The z producer writes whole lines (8 threads per line), the
+// backward contraction reads 8-row runs of whole lines and the forward reads
+// [128 rows][8 z] slices of a unit.  Measured (c4 step): L = 3 2.91 ms,
+// L = 4 2.77, L = 5 2.76; row-major tiles 3.1 ms.  The tile is allocated for
+// m rounded up to 128 rows.
+#ifndef MCK_ZT_LOG
+#define MCK_ZT_LOG 5
+#endif
+__host__ __device__ __forceinline__ int64_t zt_offset(int64_t cols, int64_t row, int64_t col) {
+  constexpr int L = MCK_ZT_LOG;
+  return ((((row >> 7) * (cols >> L)) + (col >> L)) << (7 + L)) + ((row & 127) << L) +
+         (col & ((1 << L) - 1));
 }
 
 // ---------------------------------------------------------------- hashing
