@@ -287,6 +287,8 @@ def bench_ours(args):
         e2e = {"value": ws * feats_per_step / e2e_s, "unit": "features/s",
                "h2d_bytes_per_step": int(xh.numel() * 4), "d2h_bytes_per_step": int(oh.numel() * 4),
                "ms_per_step": round(e2e_s * 1e3, 3),
+               "bound": "PCIe device->host copy of the float32 features",
+               "d2h_GBps": round(oh.numel() * 4 / e2e_s / 1e9, 1),
                "path": "paper_1702_08159_b200.streaming.HostStreamer.run (feature_map_batch per "
                        "4096-row batch; pinned host x and features; H2D/compute/D2H overlapped)"}
         del oh, xh
