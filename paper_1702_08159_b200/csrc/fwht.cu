@@ -71,7 +71,6 @@ __device__ __forceinline__ void store_row_L(V* row, uint32_t tid, const V (&v)[C
 
 template <class C>
 constexpr int rows_per_cta() { return C::T >= 256 ? 1 : 256 / C::T; }
-
 template <class C, class V>
 __global__ void __launch_bounds__(C::T * rows_per_cta<C>())
 fwht_rows_kernel(V* __restrict__ data, int64_t rows) {
@@ -212,8 +211,11 @@ int launch_cols(V* data, int64_t rows, int logn1, int n2, cudaStream_t st) {
 // reading the peers' shared memory through DSMEM (16-byte loads) and writing
 // all K output segments of its share.  A second cluster barrier keeps every
 // CTA's shared memory alive until the peers have read it.
+#ifndef MCK_CLUSTER_MINB
+#define MCK_CLUSTER_MINB 3  // 40 registers: 3 CTAs per SM (2^15: 0.68 -> 0.73 of HBM)
+#endif
 template <int K>
-__global__ void __launch_bounds__(RowCfg<14, 5>::T)
+__global__ void __launch_bounds__(RowCfg<14, 5>::T, MCK_CLUSTER_MINB)
 fwht_cluster_kernel(float* __restrict__ data, int64_t rows) {
   using C = RowCfg<14, 5>;
   constexpr int VW = K >= 16 ? 2 : 4;  // K vectors in registers
