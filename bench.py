@@ -369,18 +369,34 @@ def extras(args, P, torch, dev, hbm, rank, ws, cpu):
             P.feature_map_batch(spec0, b0, x0, out=o0[k % 4])
     graph.replay()
     g_ms = timed(graph.replay, 10, torch, ws, dev) / 20
+    # the same 20 independent batches on two streams (fork/join inside one
+    # graph), so one batch's ramp-up overlaps the other's tail
+    s2 = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    graph2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph2, stream=side):
+        for q in s2:
+            q.wait_stream(side)
+        for k in range(20):
+            with torch.cuda.stream(s2[k % 2]):
+                P.feature_map_batch(spec0, b0, x0, out=o0[k % 4])
+        for q in s2:
+            side.wait_stream(q)
+    graph2.replay()
+    g2_ms = timed(graph2.replay, 10, torch, ws, dev) / 20
     bpr0 = 784 * 4 + 16384 * 4
-    gbs0 = 1000 * bpr0 / (g_ms / 1e3) / 1e9
+    gbs0 = 1000 * bpr0 / (min(g_ms, g2_ms) / 1e3) / 1e9
     out["c0"] = {"workload": "RBF sigma=1, E=8, 1000x784 -> 16384 features/row per rank",
                  "ms_per_batch_single_launch": round(one_ms, 4),
-                 "ms_per_batch_steady": round(g_ms, 4),
-                 "features_per_s": ws * 1000 * 16384 / (g_ms / 1e3),
+                 "ms_per_batch_steady_one_stream": round(g_ms, 4),
+                 "ms_per_batch_steady": round(min(g_ms, g2_ms), 4),
+                 "features_per_s": ws * 1000 * 16384 / (min(g_ms, g2_ms) / 1e3),
                  "roofline": {"bound": "hbm", "kernel": "k_fastfood_pair (n=1024)",
                               "achieved": round(gbs0, 1), "peak": hbm, "unit": "GB/s",
                               "frac": round(gbs0 / hbm, 4),
                               "alg_bytes_per_batch": 1000 * bpr0,
-                              "method": "graph of 20 back-to-back batches, 4 rotating outputs"}}
-    del o0, graph
+                              "method": "graph of 20 independent back-to-back batches, 4 rotating "
+                                        "outputs; best of one stream and two streams"}}
+    del o0, graph, graph2
     if cpu:
         out["c0"]["cpu_baseline"] = cpu_features(spec0, synthetic.image_rows(1000, 784, 1234), cores)
 
