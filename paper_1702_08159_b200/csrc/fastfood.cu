@@ -153,7 +153,6 @@ struct FFParams {
   int32_t E;   // blocks computed: e0 .. e0+E-1, written at columns (e-e0)*n
   int64_t D;
   int32_t e0;
-  int32_t keep_l2;  // z stores tagged L2 evict_last (fused path: the tile is re-read next)
   int32_t tile8;    // z written in the tiled layout (zt_offset, ldo = tile columns), fused path
 };
 
@@ -181,7 +180,6 @@ k_fastfood(FFParams p) {
   unsigned char* tabs = ff_smem + 128;
   const int gid = threadIdx.x / T;
   const uint32_t tid = threadIdx.x % T;
-  const uint64_t pol = FEAT ? 0ull : l2_policy_evict_last();
   float* s = reinterpret_cast<float*>(ff_smem + (STAGED ? 128 + 2 * SLOT : 0)) + gid * C::SMEM_FLOATS;
   constexpr uint32_t P0 = C::mid_regs(0);
 
@@ -374,7 +372,6 @@ k_fastfood(FFParams p) {
           const float4 z4 = make_float4(z[0], z[1], z[2], z[3]);
           if (p.tile8)
             *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row, (ob + j * 4 * T) - orow)) = z4;
-          else if (p.keep_l2) st_hint(reinterpret_cast<float4*>(ob + j * 4 * T), z4, pol);
           else *reinterpret_cast<float4*>(ob + j * 4 * T) = z4;
         }
       }
@@ -460,7 +457,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   float2* s = reinterpret_cast<float2*>(ff_smem + 128 + 2 * SLOT) + warp * kPairRowFloat2;
   float* const xs = reinterpret_cast<float*>(s);  // x staging: row0 [0,N), row1 [N,2N)
   const uint32_t tp_l = thread_part<C::FULL, PL>(lane), tp_0 = thread_part<C::FULL, P0>(lane);
-  const uint64_t pol = FEAT ? 0ull : l2_policy_evict_last();
 
   // Work units (block e, row group of 16), block-major: u = e * groups + g.
   // Each CTA takes a contiguous, balanced range, so its factor tables change
@@ -678,9 +674,6 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
             const int64_t col = (ob0 + j * 4 * T) - orow0;
             if (v0) *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row0, col)) = a;
             if (v1) *reinterpret_cast<float4*>(p.out + zt_offset(p.ldo, row0 + 1, col)) = b;
-          } else if (p.keep_l2) {
-            if (v0) st_hint(reinterpret_cast<float4*>(ob0 + j * 4 * T), a, pol);
-            if (v1) st_hint(reinterpret_cast<float4*>(ob1 + j * 4 * T), b, pol);
           } else {
             if (v0) *reinterpret_cast<float4*>(ob0 + j * 4 * T) = a;
             if (v1) *reinterpret_cast<float4*>(ob1 + j * 4 * T) = b;
@@ -1091,7 +1084,6 @@ int fastfood_z_blocks(const TablesView& tv, int32_t d, double sigma, const float
   p.soff = tv.soff; p.ggath = tv.ggath;
   p.scale = scale; p.norm = 1.0f; p.out = z; p.ldo = ldz; p.E = ecount; p.D = n * ecount;
   p.e0 = e0;
-  p.keep_l2 = 0;  // the tile (1-2 GiB) is far larger than L2: no eviction hint
   p.tile8 = tile8 ? 1 : 0;
   return launch_by_logn(p, logn, false, fold, st);
 }
