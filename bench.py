@@ -184,10 +184,16 @@ def bench_ours(args):
     from paper_1702_08159_b200 import synthetic
     from paper_1702_08159_b200.streaming import HostStreamer
 
-    rank, local, ws = dist_setup("nccl")
+    # MCK_BENCH_BACKEND=gloo MCK_BENCH_SAME_DEVICE=1: code-path check of the
+    # multi-rank legs on a one-GPU box (every rank on cuda:0, host-mediated
+    # collectives; the numbers are not a scaling measurement)
+    backend = os.environ.get("MCK_BENCH_BACKEND", "nccl")
+    rank, local, ws = dist_setup(backend)
+    if os.environ.get("MCK_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if rank == 0 and ws > 1:
-        print(f"[bench] world_size={ws} backend=nccl", file=sys.stderr, flush=True)
+        print(f"[bench] world_size={ws} backend={backend}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     hbm, peak_kind, peak_json = peaks()
 

@@ -35,8 +35,14 @@ namespace mck {
 
 namespace {
 
-constexpr int kCcWarps = 14;    // warps per CTA (one CTA per SM)
-constexpr int kCcStages = 3;    // cp.async ring depth per warp
+#ifndef MCK_FWD_WARPS
+#define MCK_FWD_WARPS 14
+#endif
+#ifndef MCK_FWD_STAGES
+#define MCK_FWD_STAGES 3
+#endif
+constexpr int kCcWarps = MCK_FWD_WARPS;    // forward: warps per CTA (one CTA per SM)
+constexpr int kCcStages = MCK_FWD_STAGES;  // forward: cp.async ring depth per warp
 constexpr int kFRows = 128;     // forward: rows per item (4 per lane)
 constexpr int kFZ = 8;          // forward: z per stage
 constexpr int kZW = 1024;       // forward: z per item (one partial-logit chunk)
