@@ -475,6 +475,7 @@ def extras(args, P, torch, dev, hbm, rank, ws, cpu):
                     "expansion) + SGD, features never written to HBM",
         "rows_per_rank": rows4, "ms_per_step": round(ms4, 3),
         "features_per_s": ws * rows4 * (1 << 20) / (ms4 / 1e3),
+        "epoch_s": round((1 << 20) / (rows4 * ws) * ms4 / 1e3, 3),   # 2^20 rows at 1024 rows/rank/step
         "build_blocks_s": round(setup4, 3),
         "allreduce": (f"{len(fc.bucket_ranges())} float32 buckets of {fc.bucket_blocks} blocks "
                       f"(+ float64 [db|loss|hits]), overlapped with the backward" if ws > 1 else None),
@@ -626,6 +627,7 @@ def cpu_c4(spec, fc, x4, y4, cores, rows=4):
     per_row = dt / rows
     return {"value": rows * (1 << 20) / dt, "unit": "features/s", "cores": cores, "kind": "port",
             "s_per_rank_step_extrapolated": round(per_row * 1024, 2),
+            "epoch_h_extrapolated": round(per_row * (1 << 20) / 3600, 2),
             "sample": f"{rows} rows x 32 blocks (n=16384), featurize + loss + sgd_step, "
                       f"extrapolated x{1024 // rows} to a 1024-row rank step"}
 
