@@ -218,3 +218,34 @@ def test_checkpoint_round_trip_gpu(cuda, tmp_path):
 
 def torch_equal(a, b):
     return bool((a == b).all().item())
+
+
+def test_bench_line_on_gpu(cuda, tmp_path):
+    """bench.py's JSON contract on a GPU (short run): headline keys, the
+    roofline / e2e / clocks objects and one leg per other config, each with
+    a roofline."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--steps", "2", "--warmup", "3",
+                        "--no-cpu", "--no-e2e"], cwd=root, capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ))
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "dtype", "config", "roofline", "clocks",
+                "gpu_launches", "extras"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["gpu_launches"] == 2 * 15 and line["value"] > 0
+    rf = line["roofline"]
+    assert rf["bound"] == "hbm" and 0 < rf["frac"] < 1.2 and rf["peak"] > 0
+    ex = line["extras"]
+    for leg in ("c0", "c1_fwht_sweep", "c3_train", "c4_fused_step"):
+        assert leg in ex, leg
+    for leg in ("c0", "c3_train", "c4_fused_step"):
+        assert ex[leg]["roofline"]["frac"] > 0
+    assert len(ex["c1_fwht_sweep"]) == 11
+    assert ex["c3_train"]["final_test_acc"] >= 0.9
