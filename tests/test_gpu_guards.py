@@ -54,7 +54,8 @@ def test_fwht_guard_bands_and_determinism(cuda, n, rows):
 
 
 @pytest.mark.parametrize("d,E,m,kern", [(784, 3, 37, "rbf"), (1000, 2, 5, "matern"),
-                                        (16384, 2, 3, "rbf"), (100, 4, 33, "rbf")])
+                                        (16384, 2, 3, "rbf"), (100, 4, 33, "rbf"),
+                                        (20000, 2, 5, "rbf")])
 def test_expansion_guard_bands_and_determinism(cuda, d, E, m, kern):
     import paper_1702_08159_b200 as P
     torch = cuda
