@@ -127,6 +127,9 @@ class FusedClassifier:
                 raise ValueError(f"output buffer must be a contiguous float64 {shape} tensor on {self.dev}")
         s = self.spec
         self._last = (xt, rows, m)
+        if m == 0 and labels is not None:  # an empty shard contributes no loss / hits
+            self.loss_sum.zero_()
+            self.hits.zero_()
         with torch.cuda.device(self.dev):
             nat.call("mck_fused_forward", nat.ptr(self.blocks.tables), s.input_dim, s.expansions,
                      float(s.kernel.sigma), nat.ptr(xt), m, self._ld(xt, m), nat.ptr(rows),

@@ -84,5 +84,8 @@ def test_fused_step_with_an_empty_shard(cuda):
     w0, b0 = fc.w.clone(), fc.b.clone()
     x = torch.randn((16, 256), device="cuda")
     y = torch.randint(0, 10, (16,), device="cuda", dtype=torch.int32)
+    fc.step(x, y, m_total=32, lr=0.1)                       # a non-empty step first
+    w0, b0 = fc.w.clone(), fc.b.clone()
     fc.step(x, y, rows=torch.zeros(0, dtype=torch.int32, device="cuda"), m_total=32, lr=0.1)
     assert torch.equal(fc.w, w0) and torch.equal(fc.b, b0)
+    assert fc.loss_sum.item() == 0.0 and fc.hits.item() == 0   # no stale loss from the last step
