@@ -27,7 +27,7 @@ from .fastfood import (
     spec_from_config,
     spec_to_config,
 )
-from .wht import BenchRecord, bench_wht, bench_wht_csv, is_power_of_two, wht_fast, wht_fast_batch
+from .wht import BenchRecord, bench_wht, bench_wht_csv, is_power_of_two, wht_fast, wht_fast_batch, wht_naive
 from .exact_kernel import KernelCheckStats, kernel_check, rbf_kernel
 from .dataio import features_to_file, read_matrix, write_matrix
 from .detrand import RandomStream, fisher_yates_permutation, fisher_yates_permutations
@@ -55,7 +55,7 @@ __all__ = [
     "build_block", "build_blocks", "blocks_from_reference", "apply_zhat", "apply_zhat_batch",
     "feature_map", "feature_map_batch", "feature_dim", "param_count",
     "spec_to_config", "spec_from_config",
-    "wht_fast", "wht_fast_batch", "is_power_of_two", "bench_wht", "bench_wht_csv", "BenchRecord",
+    "wht_fast", "wht_fast_batch", "wht_naive", "is_power_of_two", "bench_wht", "bench_wht_csv", "BenchRecord",
     "kernel_check", "rbf_kernel", "KernelCheckStats",
     "features_to_file", "read_matrix", "write_matrix", "save_model", "load_model",
     "FusedClassifier",

@@ -71,6 +71,19 @@ class RandomStream:
         self.counter += count
         return out
 
+    def uniform01(self) -> float:
+        """One uniform in [0, 1) (detrand.py:136-137)."""
+        return float(self.uniform01_array(1)[0].item())
+
+    def sign_pm1(self) -> float:
+        """One +-1 draw (detrand.py:144-145)."""
+        return float(self.sign_array(1)[0].item())
+
+    def gaussian(self) -> float:
+        """One standard normal, sharing the pair cache with gaussian_array
+        (detrand.py:152-153)."""
+        return float(self.gaussian_array(1)[0].item())
+
     def gaussian_array(self, count: int):
         """detrand.py:155-171 with the cached second variate."""
         torch = self._torch()

@@ -126,6 +126,23 @@ def _naive_gpu(torch, v):
     return out
 
 
+def wht_naive(v):
+    """Transform by explicit +-1 matrix product in float64 (wht.py:67-87), on
+    the GPU: a vector of length n or an (n, k) matrix of k column vectors;
+    returns a new float64 array (numpy in -> numpy out)."""
+    torch = nat.require_cuda()
+    host = not isinstance(v, torch.Tensor)
+    t = torch.from_numpy(np.asarray(v, dtype=np.float64)) if host else v
+    single = t.dim() == 1
+    if t.dim() not in (1, 2):
+        raise ValueError("wht_naive expects a vector or an (n, k) matrix")
+    _check_pow2(int(t.shape[0]))
+    t = t.to(device="cuda", dtype=torch.float64)
+    out = _naive_gpu(torch, t if not single else t[:, None])
+    out = out[:, 0] if single else out
+    return out.cpu().numpy() if host else out
+
+
 def bench_wht(sizes, repetitions: int = 5, naive_cutoff: int = 1 << 16, dtype=np.float32):
     """Median device time per single-vector transform (CUDA events), Table-1 style.
 

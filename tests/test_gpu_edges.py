@@ -89,3 +89,22 @@ def test_fused_step_with_an_empty_shard(cuda):
     fc.step(x, y, rows=torch.zeros(0, dtype=torch.int32, device="cuda"), m_total=32, lr=0.1)
     assert torch.equal(fc.w, w0) and torch.equal(fc.b, b0)
     assert fc.loss_sum.item() == 0.0 and fc.hits.item() == 0   # no stale loss from the last step
+
+
+def test_wht_naive_and_scalar_draws(cuda):
+    """wht_naive (wht.py:67-87) against the oracle's float64 product, and the
+    scalar draws of RandomStream (detrand.py:136-153) against its arrays."""
+    import paper_1702_08159_b200 as P
+    from oracle import wht as ow
+    v = np.random.default_rng(3).standard_normal((256, 3))
+    got = P.wht_naive(v)
+    np.testing.assert_allclose(got, ow.wht_naive(v), rtol=1e-12, atol=1e-10)
+    assert P.wht_naive(v[:, 0]).shape == (256,)
+    a, b = P.RandomStream(42, "u", 3), P.RandomStream(42, "u", 3)
+    arr = a.uniform01_array(5).cpu().numpy()
+    assert [b.uniform01() for _ in range(5)] == arr.tolist()
+    a, b = P.RandomStream(7, "g"), P.RandomStream(7, "g")
+    arr = a.gaussian_array(5).cpu().numpy()         # pair cache shared with gaussian()
+    assert [b.gaussian() for _ in range(5)] == arr.tolist()
+    a, b = P.RandomStream(9, "s"), P.RandomStream(9, "s")
+    assert [b.sign_pm1() for _ in range(4)] == a.sign_array(4).cpu().numpy().tolist()
