@@ -400,7 +400,14 @@ __device__ __forceinline__ void st_out(float4* p, float4 v) { *p = v; }
 // layouts L and P0); Pi uses 16-colour slots.
 __host__ __device__ constexpr uint32_t pad2(uint32_t i) { return i + (i >> 4) + 4 * (i >> 7); }
 constexpr int kPairRowFloat2 = 1116;  // pad2(1023) + 1, rounded to 16 bytes
-constexpr int kPairWarps = 8;
+#ifndef MCK_PAIR_WARPS
+#define MCK_PAIR_WARPS 8
+#endif
+#ifndef MCK_PAIR_MINB
+#define MCK_PAIR_MINB 2
+#endif
+constexpr int kPairWarps = MCK_PAIR_WARPS;
+constexpr int kPairHdr = ((2 + kPairWarps) * 8 + 127) / 128 * 128;  // mbarriers, 128-byte aligned
 
 template <int R, uint32_t P, uint32_t ACTIVE>
 __device__ __forceinline__ void butterflies2(float2 (&v)[R]) {
@@ -435,11 +442,11 @@ template <class C>
 constexpr int pair_tab_slot() { return (pair_tab_bytes<C>() + 127) & ~127; }
 template <class C>
 constexpr size_t ff_pair_smem_bytes() {
-  return 128 + 2 * (size_t)pair_tab_slot<C>() + (size_t)kPairWarps * kPairRowFloat2 * 8;
+  return kPairHdr + 2 * (size_t)pair_tab_slot<C>() + (size_t)kPairWarps * kPairRowFloat2 * 8;
 }
 
 template <bool FEAT, bool FOLD, bool VEC>
-__global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p) {
+__global__ void __launch_bounds__(kPairWarps * 32, MCK_PAIR_MINB) k_fastfood_pair(FFParams p) {
   using C = RowCfg<10, 5>;
   constexpr int R = C::R, T = C::T, N = C::N;
   constexpr int ROWS = 2 * kPairWarps;
@@ -450,11 +457,11 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) k_fastfood_pair(FFParams p
   extern __shared__ __align__(128) unsigned char ff_smem[];
   // header: table barriers [0,1], per-warp x barriers [2 .. 2+kPairWarps)
   uint64_t* bar = reinterpret_cast<uint64_t*>(ff_smem);
-  unsigned char* tabs = ff_smem + 128;
+  unsigned char* tabs = ff_smem + kPairHdr;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   uint64_t* xbar = bar + 2 + warp;
-  float2* s = reinterpret_cast<float2*>(ff_smem + 128 + 2 * SLOT) + warp * kPairRowFloat2;
+  float2* s = reinterpret_cast<float2*>(ff_smem + kPairHdr + 2 * SLOT) + warp * kPairRowFloat2;
   float* const xs = reinterpret_cast<float*>(s);  // x staging: row0 [0,N), row1 [N,2N)
   const uint32_t tp_l = thread_part<C::FULL, PL>(lane), tp_0 = thread_part<C::FULL, P0>(lane);
 
