@@ -141,9 +141,12 @@ def test_fused_training_trajectory_vs_oracle(cuda):
     from paper_1702_08159_b200.large_scale import FusedClassifier
     torch = cuda
     spec = P.FeatureMapSpec(3000, 4, P.RBF(4.0), 77)          # n = 4096, 32768 features
-    x, y = synthetic.class_images(1200, 3000, 10, seed=5, sample_seed=6, noise=0.3)
-    xt, yt = synthetic.class_images(400, 3000, 10, seed=5, sample_seed=7, noise=0.3)
-    lr, batch, epochs = 0.5, 100, 2                           # 12 steps/epoch, 24 steps
+    # noisy classes and a small step: the loss goes 2.07 -> 0.19 and test
+    # accuracy stays near 87 % (neither saturated nor degenerate)
+    x, y = synthetic.class_images(1200, 3000, 10, seed=5, sample_seed=6, noise=1.0)
+    # 1,000 test rows: 0.2 percentage points = 2 rows
+    xt, yt = synthetic.class_images(1000, 3000, 10, seed=5, sample_seed=7, noise=1.0)
+    lr, batch, epochs = 0.02, 100, 2                          # 12 steps/epoch, 24 steps
     ospec = off.OSpec.of(spec)
     ob = off.build_blocks(ospec)
     w_ref, b_ref, hist = olm.train(ospec, x, y, xt, yt, 10, lr, batch, epochs, blocks=ob)
@@ -170,6 +173,7 @@ def test_fused_training_trajectory_vs_oracle(cuda):
     assert abs(acc - hist[-1][2]) <= 0.002 + 1e-12, (acc, hist[-1][2])
     # float32 W vs the float64 reference W: relative drift after 24 steps
     drift = np.abs(fc.w.double().cpu().numpy() - w_ref).max() / np.abs(w_ref).max()
+    print(f"fused training: losses {losses} vs {[h[1] for h in hist]}; float32-W drift {drift:.3e}")
     assert drift <= 1e-4, drift
     np.testing.assert_allclose(fc.b.cpu().numpy(), b_ref, rtol=1e-4, atol=1e-7)
 
