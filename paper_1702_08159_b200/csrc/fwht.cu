@@ -17,6 +17,7 @@
 //   fp32 sum over k of H[k][j]*x_k, then combine stages (a+b, (a+b)-2b).
 #include "mck_common.cuh"
 #include "fwht_core.cuh"
+#include "umma.cuh"
 
 #include <cooperative_groups.h>
 
@@ -319,6 +320,135 @@ int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
   }
 }
 
+// n = NSEG * 2^14, NSEG = 2 or 4 (fp32): the whole row stays on ONE SM, one
+// HBM pass, no cluster.  A persistent CTA of 512 threads walks its rows; each
+// 2^14-segment goes through the register/shared-memory transform of the row
+// kernel and is then parked in tensor memory -- the CTA owns all of the SM's
+// TMEM (NSEG * 64 KB of the 256 KB), used here as a thread-private register
+// extension: thread t of warp w writes its 32 registers to TMEM lane
+// 32*(w%4)+t, columns (w/4)*32*NSEG + 32*s.  Every thread holds the same
+// positions of every segment, so H_NSEG across the segments needs no exchange
+// at all: read the NSEG segments' values back (tcgen05.ld), butterfly, store
+// 16 bytes per segment.  The next segment's global loads are issued into a
+// second register set before the current segment is transformed, across row
+// boundaries too, so HBM reads stay in flight under the arithmetic.
+#ifndef MCK_FWHT_TMEM
+#define MCK_FWHT_TMEM 1
+#endif
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32], int o) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[o + 0])), "r"(__float_as_uint(v[o + 1])), "r"(__float_as_uint(v[o + 2])),
+      "r"(__float_as_uint(v[o + 3])), "r"(__float_as_uint(v[o + 4])), "r"(__float_as_uint(v[o + 5])),
+      "r"(__float_as_uint(v[o + 6])), "r"(__float_as_uint(v[o + 7])), "r"(__float_as_uint(v[o + 8])),
+      "r"(__float_as_uint(v[o + 9])), "r"(__float_as_uint(v[o + 10])), "r"(__float_as_uint(v[o + 11])),
+      "r"(__float_as_uint(v[o + 12])), "r"(__float_as_uint(v[o + 13])), "r"(__float_as_uint(v[o + 14])),
+      "r"(__float_as_uint(v[o + 15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int NSEG>
+__global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
+fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
+  using C = RowCfg<14, 5>;
+  constexpr int SEG = C::N;
+  constexpr uint32_t COLS = 32 * NSEG * (C::T / 128);  // 32 columns per thread and segment
+  static_assert(COLS <= 512 && (COLS & (COLS - 1)) == 0, "TMEM columns");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) umma::tmem_alloc<COLS>(&tmem_slot);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * (32u * NSEG);
+
+  float v[C::R], w[C::R];
+  int64_t row = blockIdx.x;
+  if (row < rows) load_row_L<C>(data + row * (int64_t)(NSEG * SEG), tid, w);
+  for (; row < rows; row += gridDim.x) {
+    float* prow = data + row * (int64_t)(NSEG * SEG);
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg) {
+#pragma unroll
+      for (int k = 0; k < C::R; ++k) v[k] = w[k];
+      if (sg + 1 < NSEG) {
+        load_row_L<C>(prow + (int64_t)(sg + 1) * SEG, tid, w);
+      } else if (row + gridDim.x < rows) {
+        load_row_L<C>(data + (row + gridDim.x) * (int64_t)(NSEG * SEG), tid, w);
+      }
+      butterflies<C::R, C::PL, C::PL>(v);
+      middle_rounds<C, 0, C::PL>(s, tid, 0, v);
+      constexpr uint32_t PM = last_mid_regs<C>();
+      sts_layout<C::R, PM>(s, thread_part<C::FULL, PM>(tid), v);
+      __syncthreads();
+      lds_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
+      __syncthreads();  // the next segment's first exchange reuses the buffer
+      tmem_st32(tbase + 32u * sg, v, 0);
+      tmem_st32(tbase + 32u * sg + 16u, v, 16);
+    }
+    umma::tmem_wait_st();
+    // H_NSEG across the segments, 8 registers (two 16-byte pieces) at a time
+#pragma unroll
+    for (int j = 0; j < C::R / 8; ++j) {
+      float a[NSEG][8];
+#pragma unroll
+      for (int sg = 0; sg < NSEG; ++sg) tmem_ld8_nowait(tbase + 32u * sg + 8u * j, a[sg]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int h = 1; h < NSEG; h <<= 1)
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg)
+          if (!(sg & h)) {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) bfly_pk(a[sg][i], a[sg][i + 1], a[sg | h][i], a[sg | h][i + 1]);
+          }
+#pragma unroll
+      for (int sg = 0; sg < NSEG; ++sg) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          float t[4] = {a[sg][4 * q], a[sg][4 * q + 1], a[sg][4 * q + 2], a[sg][4 * q + 3]};
+          Vec4<float>::store(prow + (int64_t)sg * SEG + 4 * tid + (size_t)(2 * j + q) * (4 * C::T), t);
+        }
+      }
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<COLS>(tmem_slot);
+}
+
+template <int NSEG>
+int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
+  using C = RowCfg<14, 5>;
+  // more than half of the SM's shared memory: one CTA per SM, which owns the TMEM
+  const size_t smem = 120 * 1024;
+  static_assert((size_t)C::SMEM_FLOATS * sizeof(float) <= 120 * 1024, "exchange buffer");
+  auto kern = fwht_tmem_kernel<NSEG>;
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "fwht tmem smem"));
+    return MCK_OK;
+  }));
+  int64_t grid = ds->sms;
+  if (grid > rows) grid = rows;
+  kern<<<(unsigned)grid, C::T, smem, st>>>(data, rows);
+  return check_launch("fwht_tmem_kernel");
+}
+
 // Second stream used to overlap phase B of chunk k with phase A of chunk k+1.
 struct SideStreams {
   cudaStream_t s[16] = {};
@@ -360,6 +490,9 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
   if constexpr (sizeof(V) == 4) {
     // (2^18 as a cluster of 16 runs on 112 SMs: 0.42 of HBM vs 0.48 for the
     // two-phase path below)
+#if MCK_FWHT_TMEM
+    if (logn == 16) return launch_tmem_t<4>(data, rows, st);
+#endif
     if (logn >= 15 && logn <= 17) return launch_cluster(data, rows, logn, st);
   }
   if (logn <= max_row_logn) return launch_rows_by_logn<V>(data, rows, logn, st);
