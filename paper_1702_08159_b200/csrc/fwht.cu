@@ -389,17 +389,18 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
         load_row_L<C>(data + (row + gridDim.x) * (int64_t)(NSEG * SEG), tid, w);
       }
       butterflies<C::R, C::PL, C::PL>(v);
+      // ends in layout PM (lanes on index bits 0..4) behind a group barrier:
+      // parked as is, no exchange back to the 16-byte layout
       middle_rounds<C, 0, C::PL>(s, tid, 0, v);
-      constexpr uint32_t PM = last_mid_regs<C>();
-      sts_layout<C::R, PM>(s, thread_part<C::FULL, PM>(tid), v);
-      __syncthreads();
-      lds_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
-      __syncthreads();  // the next segment's first exchange reuses the buffer
       tmem_st32(tbase + 32u * sg, v, 0);
       tmem_st32(tbase + 32u * sg + 16u, v, 16);
     }
     umma::tmem_wait_st();
-    // H_NSEG across the segments, 8 registers (two 16-byte pieces) at a time
+    // H_NSEG across the segments, 8 registers at a time; a warp instruction
+    // stores 128 contiguous bytes (register k of layout PM sits at element
+    // tpart | deposit(k, PM))
+    constexpr uint32_t PM = last_mid_regs<C>();
+    float* pt = prow + thread_part<C::FULL, PM>(tid);
 #pragma unroll
     for (int j = 0; j < C::R / 8; ++j) {
       float a[NSEG][8];
@@ -417,10 +418,8 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
 #pragma unroll
       for (int sg = 0; sg < NSEG; ++sg) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          float t[4] = {a[sg][4 * q], a[sg][4 * q + 1], a[sg][4 * q + 2], a[sg][4 * q + 3]};
-          Vec4<float>::store(prow + (int64_t)sg * SEG + 4 * tid + (size_t)(2 * j + q) * (4 * C::T), t);
-        }
+        for (int i = 0; i < 8; ++i)
+          pt[(int64_t)sg * SEG + deposit_bits((uint32_t)(8 * j + i), PM)] = a[sg][i];
       }
     }
   }
@@ -492,6 +491,9 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
     // two-phase path below)
 #if MCK_FWHT_TMEM
     if (logn == 16) return launch_tmem_t<4>(data, rows, st);
+#ifdef MCK_FWHT_TMEM15
+    if (logn == 15) return launch_tmem_t<2>(data, rows, st);
+#endif
 #endif
     if (logn >= 15 && logn <= 17) return launch_cluster(data, rows, logn, st);
   }
