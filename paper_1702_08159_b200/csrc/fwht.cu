@@ -335,6 +335,12 @@ int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
 #ifndef MCK_FWHT_TMEM
 #define MCK_FWHT_TMEM 1
 #endif
+#ifndef MCK_FWHT_2BUF
+#define MCK_FWHT_2BUF 1  // alternate two exchange buffers (one barrier per exchange)
+#endif
+#ifndef MCK_FWHT_TMEM_CLUSTER_MAX
+#define MCK_FWHT_TMEM_CLUSTER_MAX 18  // largest log2 n on the TMEM cluster kernel (2^19, 2^20: two-phase path is faster)
+#endif
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32], int o) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
@@ -357,6 +363,59 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Phase 1 of the TMEM kernels: transform the NSEG segments of the chunk at
+// `chunk` (segment 0 already in w) and park them; the loads of the following
+// segment -- or of segment 0 of `next` (may be null) -- fly meanwhile.
+constexpr int TMEM_S_FLOATS = (RowCfg<14, 5>::SMEM_FLOATS + 3) / 4 * 4;
+
+template <int NSEG>
+__device__ __forceinline__ void tmem_park_chunk(float* s, float* s2, uint32_t tid, uint32_t tbase,
+                                                const float* chunk, const float* next,
+                                                float (&w)[RowCfg<14, 5>::R]) {
+  using C = RowCfg<14, 5>;
+  float v[C::R];
+#pragma unroll
+  for (int sg = 0; sg < NSEG; ++sg) {
+#pragma unroll
+    for (int k = 0; k < C::R; ++k) v[k] = w[k];
+    if (sg + 1 < NSEG) {
+      load_row_L<C>(chunk + (int64_t)(sg + 1) * C::N, tid, w);
+    } else if (next) {
+      load_row_L<C>(next, tid, w);
+    }
+    butterflies<C::R, C::PL, C::PL>(v);
+    // ends in layout PM (lanes on index bits 0..4): parked as is, no
+    // exchange back to the 16-byte layout
+#if MCK_FWHT_2BUF
+    middle_rounds_2buf<C, 0, C::PL>(s, s2, tid, 0, v);
+#else
+    middle_rounds<C, 0, C::PL>(s, tid, 0, v);
+#endif
+    tmem_st32(tbase + 32u * sg, v, 0);
+    tmem_st32(tbase + 32u * sg + 16u, v, 16);
+    // re-align the warps: the next segment's loads then go out as one burst
+    // (measured: 2^15 0.83 -> 0.86 of HBM)
+    __syncthreads();
+  }
+  umma::tmem_wait_st();
+}
+
+// Eight parked registers (8j .. 8j+7) of every segment, H_NSEG applied.
+template <int NSEG>
+__device__ __forceinline__ void tmem_piece(uint32_t tbase, int j, float (&a)[NSEG][8]) {
+#pragma unroll
+  for (int sg = 0; sg < NSEG; ++sg) tmem_ld8_nowait(tbase + 32u * sg + 8u * j, a[sg]);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int h = 1; h < NSEG; h <<= 1)
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg)
+      if (!(sg & h)) {
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) bfly_pk(a[sg][i], a[sg][i + 1], a[sg | h][i], a[sg | h][i + 1]);
+      }
+}
+
 template <int NSEG>
 __global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
 fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
@@ -374,28 +433,13 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
   umma::fence_after();
   const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * (32u * NSEG);
 
-  float v[C::R], w[C::R];
+  float w[C::R];
   int64_t row = blockIdx.x;
   if (row < rows) load_row_L<C>(data + row * (int64_t)(NSEG * SEG), tid, w);
   for (; row < rows; row += gridDim.x) {
     float* prow = data + row * (int64_t)(NSEG * SEG);
-#pragma unroll
-    for (int sg = 0; sg < NSEG; ++sg) {
-#pragma unroll
-      for (int k = 0; k < C::R; ++k) v[k] = w[k];
-      if (sg + 1 < NSEG) {
-        load_row_L<C>(prow + (int64_t)(sg + 1) * SEG, tid, w);
-      } else if (row + gridDim.x < rows) {
-        load_row_L<C>(data + (row + gridDim.x) * (int64_t)(NSEG * SEG), tid, w);
-      }
-      butterflies<C::R, C::PL, C::PL>(v);
-      // ends in layout PM (lanes on index bits 0..4) behind a group barrier:
-      // parked as is, no exchange back to the 16-byte layout
-      middle_rounds<C, 0, C::PL>(s, tid, 0, v);
-      tmem_st32(tbase + 32u * sg, v, 0);
-      tmem_st32(tbase + 32u * sg + 16u, v, 16);
-    }
-    umma::tmem_wait_st();
+    const int64_t nrow = row + gridDim.x;
+    tmem_park_chunk<NSEG>(s, s + TMEM_S_FLOATS, tid, tbase, prow, nrow < rows ? data + nrow * (int64_t)(NSEG * SEG) : nullptr, w);
     // H_NSEG across the segments, 8 registers at a time; a warp instruction
     // stores 128 contiguous bytes (register k of layout PM sits at element
     // tpart | deposit(k, PM))
@@ -404,17 +448,7 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
 #pragma unroll
     for (int j = 0; j < C::R / 8; ++j) {
       float a[NSEG][8];
-#pragma unroll
-      for (int sg = 0; sg < NSEG; ++sg) tmem_ld8_nowait(tbase + 32u * sg + 8u * j, a[sg]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int h = 1; h < NSEG; h <<= 1)
-#pragma unroll
-        for (int sg = 0; sg < NSEG; ++sg)
-          if (!(sg & h)) {
-#pragma unroll
-            for (int i = 0; i < 8; i += 2) bfly_pk(a[sg][i], a[sg][i + 1], a[sg | h][i], a[sg | h][i + 1]);
-          }
+      tmem_piece<NSEG>(tbase, j, a);
 #pragma unroll
       for (int sg = 0; sg < NSEG; ++sg) {
 #pragma unroll
@@ -431,9 +465,10 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
 template <int NSEG>
 int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   using C = RowCfg<14, 5>;
-  // more than half of the SM's shared memory: one CTA per SM, which owns the TMEM
-  const size_t smem = 120 * 1024;
-  static_assert((size_t)C::SMEM_FLOATS * sizeof(float) <= 120 * 1024, "exchange buffer");
+  // two exchange buffers, more than half of the SM's shared memory: one CTA
+  // per SM, which owns the TMEM
+  const size_t smem = 2 * (size_t)TMEM_S_FLOATS * sizeof(float);
+  static_assert(2 * (size_t)TMEM_S_FLOATS * sizeof(float) > 116 * 1024, "one CTA per SM");
   auto kern = fwht_tmem_kernel<NSEG>;
   static PerDevice pd;
   const DeviceSlot* ds = nullptr;
@@ -446,6 +481,274 @@ int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   if (grid > rows) grid = rows;
   kern<<<(unsigned)grid, C::T, smem, st>>>(data, rows);
   return check_launch("fwht_tmem_kernel");
+}
+
+// n = K * 2^16, K = 2..16 (fp32): one cluster of K CTAs per row, one HBM
+// pass.  CTA c owns the contiguous 2^16 chunk c (four 2^14 segments).  After
+// a segment's register/shared-memory transform, H_K across the chunks runs at
+// equal chunk offsets and every thread keeps its element positions: of its 32
+// registers, the 32/K that peer k owns are pushed straight from the registers
+// into peer k's receive buffer (st.async through DSMEM, completing on the
+// peer's mbarrier).  One segment later -- the pushes have flown under the
+// next segment's transform -- the thread collects its own 32/K positions of
+// all K chunks, applies H_K and parks the 32 values in tensor memory.  After
+// four segments the row closes like the one-SM kernel: H_4 across the parked
+// segments and 128-byte warp stores, now into all K chunks.  Two receive
+// buffers; the pushes of segment g+2 wait for every CTA to have read segment
+// g (split cluster barrier, arrived a whole segment earlier).
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async4(uint32_t addr, uint32_t bar, float a, float b, float c, float d) {
+  asm volatile(
+      "st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(addr),
+      "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d)),
+      "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void st_async2(uint32_t addr, uint32_t bar, float a, float b) {
+  asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1,%2}, [%3];" ::"r"(addr),
+               "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int K>
+struct TmemCluster {
+  using C = RowCfg<14, 5>;
+  static constexpr int V = 32 / K;             // values per thread, piece and owner
+  static constexpr int VW = V >= 4 ? 4 : 2;    // vector width of a push
+  static constexpr int NV = V / VW;            // pushes per owner
+  static constexpr uint32_t PIECE_BYTES = 32u * C::T * 4u;  // 64 KB: K sources x V values x T threads
+  static constexpr size_t S_BYTES = ((size_t)C::SMEM_FLOATS * 4 + 15) / 16 * 16;
+  static constexpr size_t SMEM = S_BYTES + 2 * (size_t)PIECE_BYTES + 16;
+  // receive buffer: [source][vector][thread]
+  __device__ static uint32_t slot(uint32_t src, int q, uint32_t tid) {
+    return ((src * NV + q) * C::T + tid) * (VW * 4u);
+  }
+};
+
+template <int K>
+__global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
+fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
+  using C = RowCfg<14, 5>;
+  using TC = TmemCluster<K>;
+  constexpr int SEG = C::N, V = TC::V, VW = TC::VW, NV = TC::NV;
+  constexpr int64_t CHUNK = 4 * SEG;
+  constexpr uint32_t PM = last_mid_regs<C>();
+  constexpr uint32_t PUSH_BYTES = TC::PIECE_BYTES / K * (K - 1);  // a CTA's own share stays local
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  unsigned char* rb = smem_raw + TC::S_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(rb + 2 * TC::PIECE_BYTES);
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
+  if (warp == 0) umma::tmem_alloc<512>(&tmem_slot);
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+    mbar_expect_tx(&full[0], PUSH_BYTES);
+    mbar_expect_tx(&full[1], PUSH_BYTES);
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  // barriers initialised cluster-wide before any push; leaves one arrival
+  // outstanding (paired with the wait in front of the first push)
+  cluster_arrive();
+  cluster_wait();
+  cluster_arrive();
+  const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * 128u;
+  const uint32_t rb_u32 = smem_u32(rb), full_u32 = smem_u32(full);
+  // this CTA owns registers c*V .. c*V+V-1 of every thread's 32 (layout PM)
+  const uint32_t own_dep = deposit_bits(c * V, PM);
+  const uint32_t tpart = thread_part<C::FULL, PM>(tid);
+
+  const int64_t nclusters = gridDim.x / K, cid = blockIdx.x / K;
+  const int64_t mine = cid < rows ? (rows - cid + nclusters - 1) / nclusters : 0;
+  float w[C::R];
+  if (mine > 0) load_row_L<C>(data + cid * (K * CHUNK) + c * CHUNK, tid, w);
+
+  // collect segment sg (buffer sg & 1): own positions of all K chunks, H_K, park
+  auto consume = [&](int sg) {
+    const uint32_t buf = (uint32_t)(sg & 1) * TC::PIECE_BYTES;
+    mbar_wait(&full[sg & 1], (uint32_t)(sg >> 1) & 1u);
+    float x[32];  // x[k * V + i]: chunk k, owned register i
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const unsigned char* at = rb + buf + TC::slot(k, q, tid);
+        if constexpr (VW == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(at);
+          x[k * V + 4 * q] = t.x; x[k * V + 4 * q + 1] = t.y; x[k * V + 4 * q + 2] = t.z; x[k * V + 4 * q + 3] = t.w;
+        } else {
+          const float2 t = *reinterpret_cast<const float2*>(at);
+          x[k * V + 2 * q] = t.x; x[k * V + 2 * q + 1] = t.y;
+        }
+      }
+    if (tid == 0) mbar_expect_tx(&full[sg & 1], PUSH_BYTES);  // re-arm for the buffer's next use
+#pragma unroll
+    for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (!(k & h)) {
+#pragma unroll
+          for (int i = 0; i < V; i += 2)
+            bfly_pk(x[k * V + i], x[k * V + i + 1], x[(k | h) * V + i], x[(k | h) * V + i + 1]);
+        }
+    // the buffer's values have been consumed: release it to the peers.  The
+    // barrier only orders these reads against later pushes (the pushed data
+    // itself is published by the mbarrier), so no release fence is needed --
+    // a fence here would wait for every global store in flight.
+    cluster_arrive_relaxed();
+    tmem_st32(tbase + 32u * sg, x, 0);
+    tmem_st32(tbase + 32u * sg + 16u, x, 16);
+  };
+
+  for (int64_t it = 0; it <= mine; ++it) {
+    const bool have = it < mine;
+    const int64_t row = cid + it * nclusters;
+    const float* chunk = data + row * (K * CHUNK) + c * CHUNK;
+#pragma unroll
+    for (int sg = 0; sg < 4; ++sg) {
+      if (have) {
+        float v[C::R];
+#pragma unroll
+        for (int k = 0; k < C::R; ++k) v[k] = w[k];
+        if (sg + 1 < 4) {
+          load_row_L<C>(chunk + (int64_t)(sg + 1) * SEG, tid, w);
+        } else if (it + 1 < mine) {
+          load_row_L<C>(chunk + nclusters * (K * CHUNK), tid, w);
+        }
+        butterflies<C::R, C::PL, C::PL>(v);
+        middle_rounds<C, 0, C::PL>(s, tid, 0, v);
+        cluster_wait();  // every CTA has read what buffer sg & 1 held
+        const uint32_t buf = (uint32_t)(sg & 1) * TC::PIECE_BYTES;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if ((uint32_t)k == c) {
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              unsigned char* at = rb + buf + TC::slot(c, q, tid);
+              const int f = k * V + q * VW;
+              if constexpr (VW == 4)
+                *reinterpret_cast<float4*>(at) = make_float4(v[f], v[f + 1], v[f + 2], v[f + 3]);
+              else
+                *reinterpret_cast<float2*>(at) = make_float2(v[f], v[f + 1]);
+            }
+          } else {
+            const uint32_t dst = map_to_cta(rb_u32 + buf, k), bar = map_to_cta(full_u32 + 8u * (sg & 1), k);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              const int f = k * V + q * VW;
+              const uint32_t at = dst + TC::slot(c, q, tid);
+              if constexpr (VW == 4)
+                st_async4(at, bar, v[f], v[f + 1], v[f + 2], v[f + 3]);
+              else
+                st_async2(at, bar, v[f], v[f + 1]);
+            }
+          }
+        }
+        if (it == 0 && sg == 0) cluster_arrive_relaxed();  // nothing to collect yet
+      }
+      if (sg > 0) {
+        if (have) consume(sg - 1);
+      } else if (it > 0) {
+        consume(3);
+        umma::tmem_wait_st();
+        // close the previous row: H_4 across its parked segments, stores
+        float* pt = data + (row - nclusters) * (K * CHUNK) + tpart + own_dep;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float a[4][8];
+          tmem_piece<4>(tbase, j, a);
+#pragma unroll
+          for (int sgo = 0; sgo < 4; ++sgo)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int m = 8 * j + i;  // parked column: chunk m / V, owned register m % V
+              pt[(int64_t)(m / V) * CHUNK + sgo * SEG + deposit_bits((uint32_t)(m % V), PM)] = a[sgo][i];
+            }
+        }
+      }
+    }
+  }
+  cluster_wait();
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<512>(tmem_slot);
+}
+
+template <int K>
+int launch_tmem_cluster_t(float* data, int64_t rows, cudaStream_t st) {
+  using C = RowCfg<14, 5>;
+  using TC = TmemCluster<K>;
+  auto kern = fwht_tmem_cluster_kernel<K>;
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot& slot) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)TC::SMEM), "fwht tmem cluster smem"));
+    if (K > 8)
+      MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                         "fwht cluster size"));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(K * 148);
+    cfg.blockDim = dim3(C::T);
+    cfg.dynamicSmemBytes = TC::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &cfg), "fwht cluster occupancy"));
+    if (n < 1) return fail_value("no %d-CTA cluster fits on this device", K);
+    slot.occ = n;  // co-resident clusters on the device
+    return MCK_OK;
+  }));
+  int64_t nc = ds->occ;
+  if (nc > rows) nc = rows;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(nc * K));
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = TC::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = K;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, data, rows), "fwht_tmem_cluster_kernel launch"));
+  return check_launch("fwht_tmem_cluster_kernel");
+}
+
+int launch_tmem_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
+  switch (logn) {
+    case 17: return launch_tmem_cluster_t<2>(data, rows, st);
+    case 18: return launch_tmem_cluster_t<4>(data, rows, st);
+    case 19: return launch_tmem_cluster_t<8>(data, rows, st);
+    case 20: return launch_tmem_cluster_t<16>(data, rows, st);
+    default: return fail_value("internal: no TMEM cluster kernel for 2^%d", logn);
+  }
 }
 
 // Second stream used to overlap phase B of chunk k with phase A of chunk k+1.
@@ -491,9 +794,8 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
     // two-phase path below)
 #if MCK_FWHT_TMEM
     if (logn == 16) return launch_tmem_t<4>(data, rows, st);
-#ifdef MCK_FWHT_TMEM15
     if (logn == 15) return launch_tmem_t<2>(data, rows, st);
-#endif
+    if (logn >= 17 && logn <= MCK_FWHT_TMEM_CLUSTER_MAX) return launch_tmem_cluster(data, rows, logn, st);
 #endif
     if (logn >= 15 && logn <= 17) return launch_cluster(data, rows, logn, st);
   }

@@ -201,6 +201,26 @@ __device__ __forceinline__ void middle_rounds(V* s, uint32_t tid, int gid, V (&v
   }
 }
 
+// Middle rounds over two alternating exchange buffers: round j uses buffer
+// j & 1, so the barrier of the following exchange also protects this one's
+// buffer and each exchange needs a single barrier.  Fast warps then run their
+// butterflies and next stores while slower warps are still loading.  Needs an
+// even number of exchanges per pass (the caller repeats passes back to back).
+template <class C, int J, uint32_t PREV, int R, class V>
+__device__ __forceinline__ void middle_rounds_2buf(V* s0, V* s1, uint32_t tid, int gid, V (&v)[R]) {
+  static_assert(C::NMID % 2 == 0, "alternating buffers need an even number of exchanges");
+  if constexpr (J < C::NMID) {
+    constexpr uint32_t PJ = C::mid_regs(J);
+    constexpr uint32_t AJ = C::mid_active(J);
+    V* s = (J & 1) ? s1 : s0;
+    sts_layout<R, PREV>(s, thread_part<C::FULL, PREV>(tid), v);
+    group_sync<C::T>(gid);
+    lds_layout<R, PJ>(s, thread_part<C::FULL, PJ>(tid), v);
+    butterflies<R, PJ, AJ>(v);
+    middle_rounds_2buf<C, J + 1, PJ, R>(s0, s1, tid, gid, v);
+  }
+}
+
 // Register mask of the last middle round (the layout the row is in after
 // middle_rounds<C, 0, ...>).
 template <class C>
