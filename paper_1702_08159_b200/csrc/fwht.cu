@@ -89,10 +89,21 @@ fwht_rows_kernel(V* __restrict__ data, int64_t rows) {
   butterflies<C::R, C::PL, C::PL>(v);
   middle_rounds<C, 0, C::PL>(s, tid, gid, v);
   constexpr uint32_t PM = last_mid_regs<C>();
-  sts_layout<C::R, PM>(s, thread_part<C::FULL, PM>(tid), v);
-  group_sync<C::T>(gid);
-  lds_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
-  store_row_L<C>(p, tid, v);
+  if constexpr (sizeof(V) == 4 && (C::LOGN == 11 || C::LOGN == 12) && (PM & 31u) == 0) {
+    // the last butterfly layout has its lanes on index bits 0..4: a warp
+    // instruction stores 128 contiguous bytes, no exchange back to layout L
+    // (measured: 2^11 1.01 -> 1.05, 2^12 0.99 -> 1.05 of the copy bandwidth;
+    // 2^13 and 2^14 lose, 0.97 -> 0.86 and 0.92 -> 0.83: four times the store
+    // instructions cost more than the exchange there)
+    V* pt = p + thread_part<C::FULL, PM>(tid);
+#pragma unroll
+    for (int k = 0; k < C::R; ++k) pt[deposit_bits((uint32_t)k, PM)] = v[k];
+  } else {
+    sts_layout<C::R, PM>(s, thread_part<C::FULL, PM>(tid), v);
+    group_sync<C::T>(gid);
+    lds_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
+    store_row_L<C>(p, tid, v);
+  }
 }
 
 template <class C, class V>

@@ -182,7 +182,8 @@ class TestWht:
             assert abs(ss - float(z[f"n{k}.sumsq"][0])) <= 1e-5 * ss
 
     def test_large_sizes_multi_row(self, cuda):
-        # 2^15..2^18: one thread-block cluster per row (DSMEM combine);
+        # 2^15, 2^16: the row on one SM (segments parked in tensor memory);
+        # 2^17, 2^18: a cluster of 2 / 4 such SMs (st.async exchange);
         # 2^19, 2^20: column pass + row pass per L2-sized chunk (5 rows = one
         # partial chunk)
         from paper_1702_08159_b200 import wht_fast_batch
@@ -193,11 +194,12 @@ class TestWht:
             _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
 
     def test_large_sizes_many_chunks(self, cuda):
-        # many rows per launch: 2^17 x 150 rows (cluster grid), 2^20 x 19
-        # rows (four 24 MiB chunks, the last one partial)
+        # many rows per launch: persistent CTAs / clusters walk several rows
+        # each (148 CTAs, 74 clusters of 2, 33 of 4), with a ragged last
+        # round; 2^20 x 19 rows = four 24 MiB chunks, the last one partial
         from paper_1702_08159_b200 import wht_fast_batch
         torch = cuda
-        for k, rows in ((17, 150), (20, 19)):
+        for k, rows in ((15, 450), (16, 301), (17, 150), (18, 70), (20, 19)):
             x = synthetic.gaussian_rows(rows, 1 << k, seed=400 + k)
             got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
             _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
