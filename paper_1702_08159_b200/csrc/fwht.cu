@@ -3,15 +3,20 @@
 // fast variant
 //   n <= 2^14 : one thread group per row (fwht_core.cuh), rows stay in
 //               registers; 16-byte coalesced global loads/stores.
-//   2^15..2^17: one thread-block cluster of K = n/2^14 CTAs per row: each CTA
-//               transforms a 2^14-segment, then H_K across the segments via
-//               DSMEM (fwht_cluster_kernel); one HBM pass.
-//   2^18..2^20: the row is viewed as [N1][2^14].  Phase A transforms the
+//   2^15, 2^16: the whole row on one SM: 2^14 segments transformed in
+//               registers / shared memory and parked in tensor memory, H_2 /
+//               H_4 across the parked segments (fwht_tmem_kernel); one HBM pass.
+//   2^17, 2^18: a cluster of 2 / 4 such SMs per row, H_K across the chunks by
+//               st.async pushes through DSMEM (fwht_tmem_cluster_kernel); one
+//               HBM pass.
+//   2^19, 2^20: the row is viewed as [N1][2^14].  Phase A transforms the
 //               N1-long columns (registers; stores tagged L2 evict_last);
 //               phase B runs the register kernel on the N1 segments.  Chunks
 //               of <= 24 MiB keep phase A's output in the 126 MB L2 for
 //               phase B, which overlaps the next chunk's phase A on a side
 //               stream.
+//   (fwht_cluster_kernel, K = n/2^14 CTAs with DSMEM loads, is the round-1
+//   path for 2^15..2^17; kept for builds with -DMCK_FWHT_TMEM=0.)
 // parity variant (verification only; bit-exact to the reference on
 //   OpenBLAS SkylakeX): every aligned base chunk (256) becomes the sequential
 //   fp32 sum over k of H[k][j]*x_k, then combine stages (a+b, (a+b)-2b).
