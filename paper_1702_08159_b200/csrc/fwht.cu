@@ -354,6 +354,9 @@ int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
 #ifndef MCK_FWHT_2BUF
 #define MCK_FWHT_2BUF 1  // alternate two exchange buffers (one barrier per exchange)
 #endif
+#ifndef MCK_FWHT_TMEM_FIRST
+#define MCK_FWHT_TMEM_FIRST 1  // one-SM TMEM kernel with H_NSEG first (no store burst at the row end)
+#endif
 #ifndef MCK_FWHT_TMEM_CLUSTER_MAX
 #define MCK_FWHT_TMEM_CLUSTER_MAX 18  // largest log2 n on the TMEM cluster kernel (2^19, 2^20: two-phase path is faster)
 #endif
@@ -478,6 +481,181 @@ fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
   if (warp == 0) umma::tmem_free<COLS>(tmem_slot);
 }
 
+// Same row-on-one-SM transform with H_NSEG FIRST (the stages commute): the
+// row arrives in NSEG pieces -- registers j*32/NSEG .. of layout L of every
+// segment, prefetched one piece per segment step -- and each piece gets H_NSEG
+// across the segments before it is parked.  A segment step then reads one
+// H_NSEG-finished segment back from TMEM, runs the register / shared-memory
+// transform and stores it straight from its last butterfly layout.  Loads (one
+// piece) and stores (one segment) are spread evenly over the steps: there is
+// no store burst at the end of the row any more.  TMEM stays exactly full: the
+// 32 columns a step's segment frees take the next row's piece, which makes the
+// parked layout alternate between segment-major (segment q register k at
+// column 32 q + k) and piece-major (segment q register P j + i at column
+// 32 j + P q + i, P = 32 / NSEG) from one row to the next.
+template <int N, int LEN>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float (&v)[LEN], int o) {
+  static_assert(N == 8 || N == 16, "columns");
+  if constexpr (N == 16) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16};" ::"r"(taddr),
+        "r"(__float_as_uint(v[o + 0])), "r"(__float_as_uint(v[o + 1])), "r"(__float_as_uint(v[o + 2])),
+        "r"(__float_as_uint(v[o + 3])), "r"(__float_as_uint(v[o + 4])), "r"(__float_as_uint(v[o + 5])),
+        "r"(__float_as_uint(v[o + 6])), "r"(__float_as_uint(v[o + 7])), "r"(__float_as_uint(v[o + 8])),
+        "r"(__float_as_uint(v[o + 9])), "r"(__float_as_uint(v[o + 10])), "r"(__float_as_uint(v[o + 11])),
+        "r"(__float_as_uint(v[o + 12])), "r"(__float_as_uint(v[o + 13])), "r"(__float_as_uint(v[o + 14])),
+        "r"(__float_as_uint(v[o + 15]))
+        : "memory");
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[o + 0])), "r"(__float_as_uint(v[o + 1])),
+                 "r"(__float_as_uint(v[o + 2])), "r"(__float_as_uint(v[o + 3])),
+                 "r"(__float_as_uint(v[o + 4])), "r"(__float_as_uint(v[o + 5])),
+                 "r"(__float_as_uint(v[o + 6])), "r"(__float_as_uint(v[o + 7]))
+                 : "memory");
+  }
+}
+template <int N, int LEN>
+__device__ __forceinline__ void tmem_ld_cols_nowait(uint32_t taddr, float (&v)[LEN], int o) {
+  static_assert(N == 8 || N == 16, "columns");
+  uint32_t r[N];
+  if constexpr (N == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15])
+        : "r"(taddr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(taddr));
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[o + i] = __uint_as_float(r[i]);
+}
+
+template <int NSEG>
+struct TmemFirst {
+  using C = RowCfg<14, 5>;
+  static constexpr int P = 32 / NSEG;  // registers per piece and segment
+  // piece j of the row at prow into w[q * P + i] (segment q, register j * P + i of layout L)
+  __device__ static void load_piece(const float* prow, int j, uint32_t tid, float (&w)[32]) {
+#pragma unroll
+    for (int q = 0; q < NSEG; ++q)
+#pragma unroll
+      for (int t = 0; t < P / 4; ++t) {
+        float x[4];
+        Vec4<float>::load(prow + (int64_t)q * C::N + 4 * tid + (size_t)(j * (P / 4) + t) * (4 * C::T), x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w[q * P + 4 * t + e] = x[e];
+      }
+  }
+  __device__ static void across_segments(float (&w)[32]) {
+#pragma unroll
+    for (int h = 1; h < NSEG; h <<= 1)
+#pragma unroll
+      for (int q = 0; q < NSEG; ++q)
+        if (!(q & h)) {
+#pragma unroll
+          for (int i = 0; i < P; i += 2)
+            bfly_pk(w[q * P + i], w[q * P + i + 1], w[(q | h) * P + i], w[(q | h) * P + i + 1]);
+        }
+  }
+  // column of (segment q, register j * P + i): segment-major (MAJ = 0) or piece-major
+  template <int MAJ>
+  __device__ static constexpr uint32_t col(int q, int j) { return MAJ == 0 ? 32 * q + P * j : 32 * j + P * q; }
+  // park piece j (already H_NSEG'ed) of a row whose layout is MAJ
+  template <int MAJ>
+  __device__ static void park_piece(uint32_t tbase, int j, const float (&w)[32]) {
+#pragma unroll
+    for (int q = 0; q < NSEG; ++q) tmem_st_cols<P>(tbase + col<MAJ>(q, j), w, q * P);
+  }
+  // read segment q of a row whose layout is MAJ into v (layout L registers)
+  template <int MAJ>
+  __device__ static void fetch_segment(uint32_t tbase, int q, float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < NSEG; ++j) tmem_ld_cols_nowait<P>(tbase + col<MAJ>(q, j), v, j * P);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  }
+};
+
+// One row whose parked layout is MAJ: NSEG segment steps; `next` (may be null)
+// is the row whose pieces are parked meanwhile (piece 0 already in w) in the
+// other layout, `after` (may be null) the row after that (its piece 0 is left
+// in w).
+template <int NSEG, int MAJ>
+__device__ __forceinline__ void tmem_first_row(float* s, float* s2, uint32_t tid, uint32_t tbase, float* prow,
+                                               const float* next, const float* after, float (&w)[32]) {
+  using C = RowCfg<14, 5>;
+  using TF = TmemFirst<NSEG>;
+  constexpr uint32_t PM = last_mid_regs<C>();
+  float* pt = prow + thread_part<C::FULL, PM>(tid);
+#pragma unroll
+  for (int sg = 0; sg < NSEG; ++sg) {
+    float v[C::R];
+    TF::template fetch_segment<MAJ>(tbase, sg, v);  // frees the segment's 32 columns ...
+    if (next) {
+      TF::across_segments(w);
+      TF::template park_piece<1 - MAJ>(tbase, sg, w);  // ... which take the next row's piece sg
+      if (sg + 1 < NSEG) TF::load_piece(next, sg + 1, tid, w);
+      else if (after) TF::load_piece(after, 0, tid, w);
+    }
+    butterflies<C::R, C::PL, C::PL>(v);
+    middle_rounds_2buf<C, 0, C::PL>(s, s2, tid, 0, v);
+#pragma unroll
+    for (int k = 0; k < C::R; ++k) pt[(int64_t)sg * C::N + deposit_bits((uint32_t)k, PM)] = v[k];
+    umma::tmem_wait_st();
+    __syncthreads();  // re-align the warps: the next piece's loads go out as one burst
+  }
+}
+
+template <int NSEG>
+__global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
+fwht_tmem_first_kernel(float* __restrict__ data, int64_t rows) {
+  using C = RowCfg<14, 5>;
+  using TF = TmemFirst<NSEG>;
+  constexpr int64_t ROW = (int64_t)NSEG * C::N;
+  constexpr uint32_t COLS = 32 * NSEG * (C::T / 128);
+  static_assert(COLS <= 512 && (COLS & (COLS - 1)) == 0, "TMEM columns");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  float* s2 = s + TMEM_S_FLOATS;
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) umma::tmem_alloc<COLS>(&tmem_slot);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * (32u * NSEG);
+
+  const int64_t step = gridDim.x;
+  int64_t row = blockIdx.x;
+  float w[32];
+  if (row < rows) {
+    // first row: all pieces, H_NSEG, parked segment-major
+#pragma unroll
+    for (int j = 0; j < NSEG; ++j) {
+      TF::load_piece(data + row * ROW, j, tid, w);
+      TF::across_segments(w);
+      TF::template park_piece<0>(tbase, j, w);
+    }
+    umma::tmem_wait_st();
+    if (row + step < rows) TF::load_piece(data + (row + step) * ROW, 0, tid, w);
+  }
+  auto at = [&](int64_t r) -> float* { return r < rows ? data + r * ROW : nullptr; };
+  for (; row < rows; row += 2 * step) {
+    tmem_first_row<NSEG, 0>(s, s2, tid, tbase, data + row * ROW, at(row + step), at(row + 2 * step), w);
+    if (row + step < rows)
+      tmem_first_row<NSEG, 1>(s, s2, tid, tbase, data + (row + step) * ROW, at(row + 2 * step), at(row + 3 * step), w);
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<COLS>(tmem_slot);
+}
+
 template <int NSEG>
 int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   using C = RowCfg<14, 5>;
@@ -485,7 +663,11 @@ int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   // per SM, which owns the TMEM
   const size_t smem = 2 * (size_t)TMEM_S_FLOATS * sizeof(float);
   static_assert(2 * (size_t)TMEM_S_FLOATS * sizeof(float) > 116 * 1024, "one CTA per SM");
+#if MCK_FWHT_TMEM_FIRST
+  auto kern = fwht_tmem_first_kernel<NSEG>;
+#else
   auto kern = fwht_tmem_kernel<NSEG>;
+#endif
   static PerDevice pd;
   const DeviceSlot* ds = nullptr;
   MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
