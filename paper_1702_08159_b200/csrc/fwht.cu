@@ -866,6 +866,7 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
       if (sg > 0) {
         if (have) consume(sg - 1);
       } else if (it > 0) {
+        if (!have) cluster_wait();  // closing round: no push waited for the previous arrival
         consume(3);
         umma::tmem_wait_st();
         // close the previous row: H_4 across its parked segments, stores
