@@ -38,7 +38,7 @@ def _bands_ok(buf):
     return bool((b[:GUARD] == SENTINEL).all() and (b[-GUARD:] == SENTINEL).all())
 
 
-@pytest.mark.parametrize("n,rows", [(4, 3), (1024, 7), (1 << 14, 3), (1 << 15, 3), (1 << 16, 2),
+@pytest.mark.parametrize("n,rows", [(4, 3), (1024, 7), (1 << 14, 3), (1 << 14, 300), (1 << 15, 3), (1 << 16, 2),
                                     (1 << 17, 3), (1 << 18, 2), (1 << 20, 1)])
 def test_fwht_guard_bands_and_determinism(cuda, n, rows):
     import paper_1702_08159_b200 as P

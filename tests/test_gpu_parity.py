@@ -194,12 +194,12 @@ class TestWht:
             _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
 
     def test_large_sizes_many_chunks(self, cuda):
-        # many rows per launch: persistent CTAs / clusters walk several rows
+        # many rows per launch (2^14 x 449: the persistent 2^14 kernel): persistent CTAs / clusters walk several rows
         # each (148 CTAs, 74 clusters of 2, 33 of 4), with a ragged last
         # round; 2^20 x 19 rows = four 24 MiB chunks, the last one partial
         from paper_1702_08159_b200 import wht_fast_batch
         torch = cuda
-        for k, rows in ((15, 450), (16, 301), (17, 150), (18, 70), (20, 19)):
+        for k, rows in ((14, 449), (15, 450), (16, 301), (17, 150), (18, 70), (20, 19)):
             x = synthetic.gaussian_rows(rows, 1 << k, seed=400 + k)
             got = wht_fast_batch(torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
             _scale_close(got, ow.wht_butterfly_f64(x.astype(np.float64)))
