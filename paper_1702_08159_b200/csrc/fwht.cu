@@ -1074,6 +1074,14 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
     if (!ev_a) rc = check_cuda(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming), "event");
     if (rc == MCK_OK) rc = check_cuda(cudaEventRecord(ev_a, st), "event");
     if (rc == MCK_OK) rc = check_cuda(cudaStreamWaitEvent(side, ev_a, 0), "wait");
+    // phase B: the persistent 2^14 kernel when the chunk has two segments per
+    // SM (2^19 0.49 -> 0.54, 2^20 0.50 -> 0.52), else one CTA per segment
+    if constexpr (sizeof(V) == 4) {
+      if (rc == MCK_OK && (nr << logn1) >= 2 * 148) {
+        rc = launch_persistent14(p, nr << logn1, side);
+        continue;
+      }
+    }
     if (rc == MCK_OK) rc = launch_rows_by_logn<V>(p, nr << logn1, logn2, side);
   }
   if (rc == MCK_OK) rc = check_cuda(cudaEventRecord(ev_b, side), "event");
