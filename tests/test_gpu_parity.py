@@ -295,6 +295,24 @@ class TestFeatures:
         zp = P.apply_zhat_batch(spec, bs, x, variant="parity")
         np.testing.assert_array_equal(zp, off.apply_zhat_batch(ospec, oblocks, x, wht="sequential"))
 
+    @pytest.mark.parametrize("cfg,m", [("c0", 1000), ("c2", 256)])
+    def test_dense_features_against_oracle(self, cuda, cfg, m):
+        # every column of every row (c0: the whole 1,000-row batch; c2: 256
+        # rows through all 16 Matern blocks) against the pinned oracle run on
+        # the GPU's factors (bit-exact to the reference's, TestFactors); the
+        # golden-fixture test above samples rows and columns of the same maps.
+        import paper_1702_08159_b200 as P
+        meta = json.loads(str(load_npz(f"{cfg}.npz")["meta"][0]))
+        spec = _spec(meta)
+        bs = P.build_blocks(spec)
+        ospec = off.OSpec.of(spec)
+        oblocks = [off.OBlock(*bs[e].numpy(), e) for e in range(spec.expansions)]
+        x = synthetic.image_rows(meta["m"], meta["d"], meta["xseed"])[:m]
+        want = off.feature_map_batch(ospec, oblocks, x)
+        got = P.feature_map_batch(spec, bs, x)
+        assert got.shape == want.shape == (m, 2 * spec.padded_dim * spec.expansions)
+        np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-6)
+
     def test_parity_variant_z_bit_exact(self, cuda):
         P, z, spec, x = self._config("c0")
         zz = P.apply_zhat_batch(spec, P.build_blocks(spec), x, variant="parity")
