@@ -771,6 +771,8 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+constexpr int kNoClusterFits = -0x4e4f;  // internal: launch_tmem_cluster could not place a cluster
+
 template <int K>
 struct TmemCluster {
   using C = RowCfg<14, 5>;
@@ -968,10 +970,10 @@ int launch_tmem_cluster_t(float* data, int64_t rows, cudaStream_t st) {
     cfg.numAttrs = 1;
     int n = 0;
     MCK_TRY(check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &cfg), "fwht cluster occupancy"));
-    if (n < 1) return fail_value("no %d-CTA cluster fits on this device", K);
-    slot.occ = n;  // co-resident clusters on the device
+    slot.occ = n;  // co-resident clusters on the device (0: none fits, e.g. a partitioned GPU)
     return MCK_OK;
   }));
+  if (ds->occ < 1) return kNoClusterFits;
   int64_t nc = ds->occ;
   if (nc > rows) nc = rows;
   cudaLaunchConfig_t cfg{};
@@ -1039,16 +1041,19 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
     return check_launch("fwht_tiny_kernel");
   }
   if constexpr (sizeof(V) == 4) {
-    // (2^18 as a cluster of 16 runs on 112 SMs: 0.42 of HBM vs 0.48 for the
-    // two-phase path below)
 #if MCK_FWHT_TMEM
     // enough rows for two per SM: the persistent kernel (0.93 -> 0.96 of HBM at 1 GiB)
     if (logn == 14 && rows >= 2 * 148) return launch_persistent14(data, rows, st);
     if (logn == 16) return launch_tmem_t<4>(data, rows, st);
     if (logn == 15) return launch_tmem_t<2>(data, rows, st);
-    if (logn >= 17 && logn <= MCK_FWHT_TMEM_CLUSTER_MAX) return launch_tmem_cluster(data, rows, logn, st);
-#endif
+    if (logn >= 17 && logn <= MCK_FWHT_TMEM_CLUSTER_MAX) {
+      // where no such cluster can be resident the two-phase path below takes over
+      const int rc = launch_tmem_cluster(data, rows, logn, st);
+      if (rc != kNoClusterFits) return rc;
+    }
+#else
     if (logn >= 15 && logn <= 17) return launch_cluster(data, rows, logn, st);
+#endif
   }
   if (logn <= max_row_logn) return launch_rows_by_logn<V>(data, rows, logn, st);
   const int logn2 = 14, logn1 = logn - logn2;
