@@ -68,6 +68,16 @@ __device__ __forceinline__ void load_row_L(const V* row, uint32_t tid, V (&v)[C:
     for (int c = 0; c < 4; ++c) v[4 * j + c] = t[c];
   }
 }
+// Same through L2 only (ld.global.cg): for kernels whose shared memory leaves
+// little L1 (the in-flight lines of a prefetched segment otherwise need L1 room).
+template <class C>
+__device__ __forceinline__ void load_row_L_cg(const float* row, uint32_t tid, float (&v)[C::R]) {
+#pragma unroll
+  for (int j = 0; j < C::R / 4; ++j) {
+    const float4 t = __ldcg(reinterpret_cast<const float4*>(row + 4 * tid + (size_t)j * (4 * C::T)));
+    v[4 * j] = t.x; v[4 * j + 1] = t.y; v[4 * j + 2] = t.z; v[4 * j + 3] = t.w;
+  }
+}
 template <class C, class V>
 __device__ __forceinline__ void store_row_L(V* row, uint32_t tid, const V (&v)[C::R]) {
 #pragma unroll
@@ -830,7 +840,7 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
   const int64_t nclusters = gridDim.x / K, cid = blockIdx.x / K;
   const int64_t mine = cid < rows ? (rows - cid + nclusters - 1) / nclusters : 0;
   float w[C::R];
-  if (mine > 0) load_row_L<C>(data + cid * (K * CHUNK) + c * CHUNK, tid, w);
+  if (mine > 0) load_row_L_cg<C>(data + cid * (K * CHUNK) + c * CHUNK, tid, w);
 
   // collect segment sg (buffer sg & 1): own positions of all K chunks, H_K, park
   auto consume = [&](int sg) {
@@ -880,9 +890,9 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
 #pragma unroll
         for (int k = 0; k < C::R; ++k) v[k] = w[k];
         if (sg + 1 < 4) {
-          load_row_L<C>(chunk + (int64_t)(sg + 1) * SEG, tid, w);
+          load_row_L_cg<C>(chunk + (int64_t)(sg + 1) * SEG, tid, w);
         } else if (it + 1 < mine) {
-          load_row_L<C>(chunk + nclusters * (K * CHUNK), tid, w);
+          load_row_L_cg<C>(chunk + nclusters * (K * CHUNK), tid, w);
         }
         butterflies<C::R, C::PL, C::PL>(v);
         middle_rounds<C, 0, C::PL>(s, tid, 0, v);
