@@ -790,12 +790,18 @@ struct TmemCluster {
   static constexpr int VW = V >= 4 ? 4 : 2;    // vector width of a push
   static constexpr int NV = V / VW;            // pushes per owner
   static constexpr uint32_t PIECE_BYTES = 32u * C::T * 4u;  // 64 KB: K sources x V values x T threads
+  static constexpr uint32_t SRC_BYTES = PIECE_BYTES / K;    // one source's share
+  static constexpr uint32_t REMOTE_BYTES = SRC_BYTES * (K - 1);
   static constexpr size_t S_BYTES = ((size_t)C::SMEM_FLOATS * 4 + 15) / 16 * 16;
-  static constexpr size_t SMEM = S_BYTES + 2 * (size_t)PIECE_BYTES + 16;
-  // receive buffer: [source][vector][thread]
-  __device__ static uint32_t slot(uint32_t src, int q, uint32_t tid) {
-    return ((src * NV + q) * C::T + tid) * (VW * 4u);
-  }
+  // one buffer for the CTA's own share (written after the previous segment's
+  // collect has read it) and two for the peers' shares (in flight under the
+  // next transform).  K = 2: 162 KB, which fits the 164 KB carve-out and
+  // leaves 92 KB of L1 for the prefetch loads (DESIGN: carve-out vs loads)
+  static constexpr size_t SMEM = S_BYTES + SRC_BYTES + 2 * (size_t)REMOTE_BYTES + 16;
+  // vector q of thread tid inside one source's share
+  __device__ static uint32_t slot(int q, uint32_t tid) { return (q * C::T + tid) * (VW * 4u); }
+  // index of source `src` among the K - 1 remote shares of CTA `dst`
+  __device__ static uint32_t remote_index(uint32_t src, uint32_t dst) { return src < dst ? src : src - 1; }
 };
 
 template <int K>
@@ -809,8 +815,9 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
   constexpr uint32_t PUSH_BYTES = TC::PIECE_BYTES / K * (K - 1);  // a CTA's own share stays local
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* s = reinterpret_cast<float*>(smem_raw);
-  unsigned char* rb = smem_raw + TC::S_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(rb + 2 * TC::PIECE_BYTES);
+  unsigned char* own = smem_raw + TC::S_BYTES;  // this CTA's own share
+  unsigned char* rb = own + TC::SRC_BYTES;      // two buffers of the peers' shares
+  uint64_t* full = reinterpret_cast<uint64_t*>(rb + 2 * TC::REMOTE_BYTES);
   __shared__ uint32_t tmem_slot;
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   uint32_t c;
@@ -844,14 +851,16 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
 
   // collect segment sg (buffer sg & 1): own positions of all K chunks, H_K, park
   auto consume = [&](int sg) {
-    const uint32_t buf = (uint32_t)(sg & 1) * TC::PIECE_BYTES;
+    const uint32_t buf = (uint32_t)(sg & 1) * TC::REMOTE_BYTES;
     mbar_wait(&full[sg & 1], (uint32_t)(sg >> 1) & 1u);
     float x[32];  // x[k * V + i]: chunk k, owned register i
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
       for (int q = 0; q < NV; ++q) {
-        const unsigned char* at = rb + buf + TC::slot(k, q, tid);
+        const unsigned char* at = (uint32_t)k == c
+                                      ? own + TC::slot(q, tid)
+                                      : rb + buf + TC::remote_index(k, c) * TC::SRC_BYTES + TC::slot(q, tid);
         if constexpr (VW == 4) {
           const float4 t = *reinterpret_cast<const float4*>(at);
           x[k * V + 4 * q] = t.x; x[k * V + 4 * q + 1] = t.y; x[k * V + 4 * q + 2] = t.z; x[k * V + 4 * q + 3] = t.w;
@@ -885,6 +894,7 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
     const float* chunk = data + row * (K * CHUNK) + c * CHUNK;
 #pragma unroll
     for (int sg = 0; sg < 4; ++sg) {
+      float keep[V];
       if (have) {
         float v[C::R];
 #pragma unroll
@@ -897,39 +907,49 @@ fwht_tmem_cluster_kernel(float* __restrict__ data, int64_t rows) {
         butterflies<C::R, C::PL, C::PL>(v);
         middle_rounds<C, 0, C::PL>(s, tid, 0, v);
         cluster_wait();  // every CTA has read what buffer sg & 1 held
-        const uint32_t buf = (uint32_t)(sg & 1) * TC::PIECE_BYTES;
+        const uint32_t buf = (uint32_t)(sg & 1) * TC::REMOTE_BYTES;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if ((uint32_t)k == c) {
+          if ((uint32_t)k == c) continue;
+          const uint32_t dst = map_to_cta(rb_u32 + buf + TC::remote_index(c, k) * TC::SRC_BYTES, k);
+          const uint32_t bar = map_to_cta(full_u32 + 8u * (sg & 1), k);
 #pragma unroll
-            for (int q = 0; q < NV; ++q) {
-              unsigned char* at = rb + buf + TC::slot(c, q, tid);
-              const int f = k * V + q * VW;
-              if constexpr (VW == 4)
-                *reinterpret_cast<float4*>(at) = make_float4(v[f], v[f + 1], v[f + 2], v[f + 3]);
-              else
-                *reinterpret_cast<float2*>(at) = make_float2(v[f], v[f + 1]);
-            }
-          } else {
-            const uint32_t dst = map_to_cta(rb_u32 + buf, k), bar = map_to_cta(full_u32 + 8u * (sg & 1), k);
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-              const int f = k * V + q * VW;
-              const uint32_t at = dst + TC::slot(c, q, tid);
-              if constexpr (VW == 4)
-                st_async4(at, bar, v[f], v[f + 1], v[f + 2], v[f + 3]);
-              else
-                st_async2(at, bar, v[f], v[f + 1]);
-            }
+          for (int q = 0; q < NV; ++q) {
+            const int f = k * V + q * VW;
+            const uint32_t at = dst + TC::slot(q, tid);
+            if constexpr (VW == 4)
+              st_async4(at, bar, v[f], v[f + 1], v[f + 2], v[f + 3]);
+            else
+              st_async2(at, bar, v[f], v[f + 1]);
           }
         }
+        // the own share, kept until the previous segment's has been read
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if ((uint32_t)k == c) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) keep[i] = v[k * V + i];
+          }
         if (it == 0 && sg == 0) cluster_arrive_relaxed();  // nothing to collect yet
       }
-      if (sg > 0) {
-        if (have) consume(sg - 1);
-      } else if (it > 0) {
+      const bool pending = sg > 0 ? have : it > 0;
+      if (pending) {
         if (!have) cluster_wait();  // closing round: no push waited for the previous arrival
-        consume(3);
+        consume((sg + 3) & 3);
+      }
+      if (have) {
+        // own share of this segment (its buffer's previous content is consumed);
+        // read back by this thread only
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          unsigned char* at = own + TC::slot(q, tid);
+          if constexpr (VW == 4)
+            *reinterpret_cast<float4*>(at) = make_float4(keep[4 * q], keep[4 * q + 1], keep[4 * q + 2], keep[4 * q + 3]);
+          else
+            *reinterpret_cast<float2*>(at) = make_float2(keep[2 * q], keep[2 * q + 1]);
+        }
+      }
+      if (sg == 0 && it > 0) {
         umma::tmem_wait_st();
         // close the previous row: H_4 across its parked segments, stores
         float* pt = data + (row - nclusters) * (K * CHUNK) + tpart + own_dep;
