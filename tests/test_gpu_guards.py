@@ -53,6 +53,30 @@ def test_fwht_guard_bands_and_determinism(cuda, n, rows):
     assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
+@pytest.mark.parametrize("k,rows", [(15, 200), (16, 160), (17, 100), (18, 40)])
+def test_fwht_two_streams_at_once(cuda, k, rows):
+    """The persistent TMEM kernels own a whole SM each (all of its tensor memory,
+    most of its shared memory): two transforms issued on two streams at once
+    must neither deadlock on the TMEM allocation / cluster barriers nor
+    disturb each other's result (bit-identical to the same call run alone)."""
+    import paper_1702_08159_b200 as P
+    torch = cuda
+    g = torch.Generator(device="cuda").manual_seed(k)
+    a = torch.randn((rows, 1 << k), generator=g, device="cuda")
+    b = torch.randn((rows, 1 << k), generator=g, device="cuda")
+    wa, wb = P.wht_fast_batch(a.clone()), P.wht_fast_batch(b.clone())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(5):
+        ca, cb = a.clone(), b.clone()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            P.wht_fast_batch(ca)
+        with torch.cuda.stream(s2):
+            P.wht_fast_batch(cb)
+        torch.cuda.synchronize()
+        assert torch.equal(ca, wa) and torch.equal(cb, wb)
+
+
 @pytest.mark.parametrize("d,E,m,kern", [(784, 3, 37, "rbf"), (1000, 2, 5, "matern"),
                                         (16384, 2, 3, "rbf"), (100, 4, 33, "rbf"),
                                         (20000, 2, 5, "rbf")])
