@@ -371,6 +371,9 @@ int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
 #ifndef MCK_FWHT_TMEM_FIRST
 #define MCK_FWHT_TMEM_FIRST 1  // one-SM TMEM kernel with H_NSEG first (no store burst at the row end)
 #endif
+#ifndef MCK_FWHT_VIRTUAL
+#define MCK_FWHT_VIRTUAL 2  // largest row / 2^16 on the virtual-row kernel (2^17: 0.71 -> 0.82; 4 = 2^18 too: 0.45 vs 0.55 with DSMEM)
+#endif
 #ifndef MCK_FWHT_TMEM_CLUSTER_MAX
 #define MCK_FWHT_TMEM_CLUSTER_MAX 18  // largest log2 n on the TMEM cluster kernel (2^19, 2^20: two-phase path is faster)
 #endif
@@ -1022,10 +1025,226 @@ int launch_tmem_cluster_t(float* data, int64_t rows, cudaStream_t st) {
   return check_launch("fwht_tmem_cluster_kernel");
 }
 
+// n = VR * 2^16, VR = 2 or 4 (fp32): "virtual rows".  H_n = H_VR (x) H_{2^16}
+// and the stages commute, so output chunk vr of a row is the 2^16 transform
+// of sum_c (-1)^popc(vr & c) x_c over the row's VR input chunks.  CTA vr of a
+// VR-CTA cluster computes exactly that: it runs the one-SM pipeline above on
+// its virtual row, whose pieces are formed at load time from the same
+// positions of ALL VR chunks (each input is read VR times, once from HBM and
+// VR - 1 times from L2: the CTAs of a cluster walk the row together).  No
+// data crosses between the SMs -- no DSMEM, no receive buffers; the cluster
+// exists for its barrier: the transform is in place, so a CTA may only store
+// its output chunk once every CTA has loaded the whole row (arrive after the
+// row's last piece is parked, wait before its first store).  A piece (8
+// registers per segment) arrives as VR sub-pieces so that 32 registers of
+// loads are in flight at a time; they are consumed at VR points spread over
+// the segment step.
+template <int N, int LEN>
+__device__ __forceinline__ void tmem_st_small(uint32_t taddr, const float (&v)[LEN], int o) {
+  static_assert(N == 2 || N == 4, "columns");
+  if constexpr (N == 4)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[o + 0])), "r"(__float_as_uint(v[o + 1])),
+                 "r"(__float_as_uint(v[o + 2])), "r"(__float_as_uint(v[o + 3]))
+                 : "memory");
+  else
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr),
+                 "r"(__float_as_uint(v[o + 0])), "r"(__float_as_uint(v[o + 1]))
+                 : "memory");
+}
+
+template <int VR>
+struct TmemVirtual {
+  using C = RowCfg<14, 5>;
+  using TF = TmemFirst<4>;
+  static constexpr int PV = 8 / VR;  // registers per segment and chunk in one sub-piece
+  static constexpr int64_t CHUNK = 4 * (int64_t)C::N;
+  // sub-piece u (piece j = u / VR, part h = u % VR) of the row at `row`:
+  // w[(c * 4 + q) * PV + e] = chunk c, segment q, register 8 j + PV h + e of layout L
+  __device__ static void load_sub(const float* row, int u, uint32_t tid, float (&w)[32]) {
+    const int k0 = 8 * (u / VR) + PV * (u % VR);
+    const size_t off = (size_t)(k0 & 3) + 4 * tid + (size_t)(k0 >> 2) * (4 * C::T);
+#pragma unroll
+    for (int c = 0; c < VR; ++c)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* p = row + c * CHUNK + (int64_t)q * C::N + off;
+        if constexpr (PV == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(p);
+          w[(c * 4 + q) * 4] = t.x; w[(c * 4 + q) * 4 + 1] = t.y; w[(c * 4 + q) * 4 + 2] = t.z; w[(c * 4 + q) * 4 + 3] = t.w;
+        } else {
+          const float2 t = *reinterpret_cast<const float2*>(p);
+          w[(c * 4 + q) * 2] = t.x; w[(c * 4 + q) * 2 + 1] = t.y;
+        }
+      }
+  }
+  // this CTA's virtual row from the raw sub-piece, then H_4 across the segments
+  __device__ static void form(const float (&w)[32], uint32_t vr, float (&d)[4 * PV]) {
+#pragma unroll
+    for (int i = 0; i < 4 * PV; ++i) d[i] = w[i];
+#pragma unroll
+    for (int c = 1; c < VR; ++c) {
+      const bool neg = __popc(vr & (uint32_t)c) & 1;
+#pragma unroll
+      for (int i = 0; i < 4 * PV; ++i) d[i] = neg ? d[i] - w[c * 4 * PV + i] : d[i] + w[c * 4 * PV + i];
+    }
+#pragma unroll
+    for (int h = 1; h < 4; h <<= 1)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!(q & h)) {
+#pragma unroll
+          for (int i = 0; i < PV; i += 2) bfly_pk(d[q * PV + i], d[q * PV + i + 1], d[(q | h) * PV + i], d[(q | h) * PV + i + 1]);
+        }
+  }
+  template <int MAJ>
+  __device__ static void park_sub(uint32_t tbase, int j, int h, const float (&d)[4 * PV]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tmem_st_small<PV>(tbase + TF::template col<MAJ>(q, j) + PV * h, d, q * PV);
+  }
+};
+
+// One virtual row parked in layout MAJ.  out: this CTA's output chunk of the
+// row; next / after: the following rows (may be null), w holds next's
+// sub-piece 0 on entry and after's on exit.
+template <int VR, int MAJ>
+__device__ __forceinline__ void tmem_virtual_row(float* s, float* s2, uint32_t tid, uint32_t vr, uint32_t tbase,
+                                                 float* out, const float* next, const float* after,
+                                                 float (&w)[32]) {
+  using C = RowCfg<14, 5>;
+  using TF = TmemFirst<4>;
+  using TV = TmemVirtual<VR>;
+  constexpr uint32_t P0 = C::mid_regs(0), PM = last_mid_regs<C>();
+  static_assert(C::NMID == 2, "two exchanges");
+  float* pt = out + thread_part<C::FULL, PM>(tid);
+#pragma unroll
+  for (int sg = 0; sg < 4; ++sg) {
+    float v[C::R];
+    TF::template fetch_segment<MAJ>(tbase, sg, v);  // frees the columns the next row's piece sg takes
+    auto service = [&](int h) {  // part h of the next row's piece sg; then the following loads
+      if (!next) return;
+      float d[4 * TV::PV];
+      TV::form(w, vr, d);
+      TV::template park_sub<1 - MAJ>(tbase, sg, h, d);
+      const int u = sg * VR + h + 1;
+      if (u < 4 * VR) TV::load_sub(next, u, tid, w);
+      else if (after) TV::load_sub(after, 0, tid, w);
+    };
+    service(0);
+    butterflies<C::R, C::PL, C::PL>(v);
+    sts_layout<C::R, C::PL>(s, thread_part<C::FULL, C::PL>(tid), v);
+    __syncthreads();
+    lds_layout<C::R, P0>(s, thread_part<C::FULL, P0>(tid), v);
+    if (VR == 4) service(1);
+    butterflies<C::R, P0, C::mid_active(0)>(v);
+    sts_layout<C::R, P0>(s2, thread_part<C::FULL, P0>(tid), v);
+    __syncthreads();
+    lds_layout<C::R, PM>(s2, thread_part<C::FULL, PM>(tid), v);
+    service(VR == 4 ? 2 : 1);
+    butterflies<C::R, PM, C::mid_active(1)>(v);
+    if (VR == 4) service(3);
+    if (sg == 3 && next) cluster_arrive_relaxed();  // this CTA has loaded the whole next row
+    if (sg == 0) cluster_wait();                    // every CTA has loaded this row: its chunks may be overwritten
+#pragma unroll
+    for (int k = 0; k < C::R; ++k) pt[(int64_t)sg * C::N + deposit_bits((uint32_t)k, PM)] = v[k];
+    umma::tmem_wait_st();
+    __syncthreads();  // re-align the warps: the next loads go out as one burst
+  }
+}
+
+template <int VR>
+__global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
+fwht_tmem_virtual_kernel(float* __restrict__ data, int64_t rows) {
+  using C = RowCfg<14, 5>;
+  using TV = TmemVirtual<VR>;
+  constexpr int64_t ROW = VR * TV::CHUNK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  float* s2 = s + TMEM_S_FLOATS;
+  __shared__ uint32_t tmem_slot;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
+  uint32_t vr;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(vr));
+  if (warp == 0) umma::tmem_alloc<512>(&tmem_slot);
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * 128u;
+
+  const int64_t nclusters = gridDim.x / VR, cid = blockIdx.x / VR;
+  const int64_t mine = cid < rows ? (rows - cid + nclusters - 1) / nclusters : 0;
+  const int64_t step = nclusters * ROW;
+  float* const row0 = data + cid * ROW;
+  float w[32];
+  if (mine > 0) {
+    // first row: every sub-piece, formed and parked segment-major
+#pragma unroll
+    for (int u = 0; u < 4 * VR; ++u) {
+      TV::load_sub(row0, u, tid, w);
+      float d[4 * TV::PV];
+      TV::form(w, vr, d);
+      TV::template park_sub<0>(tbase, u / VR, u % VR, d);
+    }
+    umma::tmem_wait_st();
+    cluster_arrive_relaxed();  // first row loaded
+    if (mine > 1) TV::load_sub(row0 + step, 0, tid, w);
+  }
+  auto at = [&](int64_t it) -> float* { return it < mine ? row0 + it * step : nullptr; };
+  for (int64_t it = 0; it < mine; it += 2) {
+    tmem_virtual_row<VR, 0>(s, s2, tid, vr, tbase, at(it) + vr * TV::CHUNK, at(it + 1), at(it + 2), w);
+    if (it + 1 < mine)
+      tmem_virtual_row<VR, 1>(s, s2, tid, vr, tbase, at(it + 1) + vr * TV::CHUNK, at(it + 2), at(it + 3), w);
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free<512>(tmem_slot);
+}
+
+template <int VR>
+int launch_tmem_virtual_t(float* data, int64_t rows, cudaStream_t st) {
+  using C = RowCfg<14, 5>;
+  const size_t smem = 2 * (size_t)TMEM_S_FLOATS * sizeof(float);
+  auto kern = fwht_tmem_virtual_kernel<VR>;
+  static PerDevice pd;
+  const DeviceSlot* ds = nullptr;
+  auto config = [&](unsigned grid, cudaLaunchAttribute* at) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(C::T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = VR;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+  };
+  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot& slot) {
+    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "fwht virtual smem"));
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = config(VR * 148, at);
+    cfg.stream = nullptr;
+    int n = 0;
+    MCK_TRY(check_cuda(cudaOccupancyMaxActiveClusters(&n, kern, &cfg), "fwht virtual occupancy"));
+    slot.occ = n;
+    return MCK_OK;
+  }));
+  if (ds->occ < 1) return kNoClusterFits;
+  int64_t nc = ds->occ;
+  if (nc > rows) nc = rows;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = config((unsigned)(nc * VR), at);
+  MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, data, rows), "fwht_tmem_virtual_kernel launch"));
+  return check_launch("fwht_tmem_virtual_kernel");
+}
+
 int launch_tmem_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
   switch (logn) {
-    case 17: return launch_tmem_cluster_t<2>(data, rows, st);
-    case 18: return launch_tmem_cluster_t<4>(data, rows, st);
+    case 17: return MCK_FWHT_VIRTUAL >= 2 ? launch_tmem_virtual_t<2>(data, rows, st) : launch_tmem_cluster_t<2>(data, rows, st);
+    case 18: return MCK_FWHT_VIRTUAL >= 4 ? launch_tmem_virtual_t<4>(data, rows, st) : launch_tmem_cluster_t<4>(data, rows, st);
     case 19: return launch_tmem_cluster_t<8>(data, rows, st);
     case 20: return launch_tmem_cluster_t<16>(data, rows, st);
     default: return fail_value("internal: no TMEM cluster kernel for 2^%d", logn);
