@@ -432,7 +432,8 @@ def extras(args, P, torch, dev, hbm, rank, ws, cpu):
         gbs = 2 ** 31 / (ms / 1e3) / 1e9
         kern = ("fwht_rows_kernel" if k <= 13 else "fwht_persistent14_kernel" if k == 14
                 else "fwht_tmem_first_kernel (row on one SM)" if k <= 16
-                else "fwht_tmem_cluster_kernel" if k <= 18 else "two-phase (columns + rows)")
+                else "fwht_tmem_virtual_kernel (two virtual rows per row)" if k == 17
+                else "fwht_tmem_cluster_kernel" if k == 18 else "two-phase (columns + rows)")
         sweep[str(n)] = {"ms": round(ms, 4), "GBps": round(gbs, 1), "frac": round(gbs / hbm, 4),
                          "rows_per_rank": hi - lo, "kernel": kern}
     del buf

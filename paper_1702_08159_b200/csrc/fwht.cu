@@ -10,7 +10,10 @@
 //               pieces parked in tensor memory; then each segment is read
 //               back, transformed in registers / shared memory and stored;
 //               one HBM pass.
-//   2^17, 2^18: a cluster of 2 / 4 such SMs per row, H_K across the chunks by
+//   2^17:       two "virtual rows" x0 + x1 and x0 - x1, formed at load time,
+//               one per SM of a 2-CTA cluster on the one-SM pipeline
+//               (fwht_tmem_virtual_kernel); one HBM pass, no DSMEM.
+//   2^18:       a cluster of 4 such SMs per row, H_4 across the chunks by
 //               st.async pushes through DSMEM (fwht_tmem_cluster_kernel); one
 //               HBM pass.
 //   2^19, 2^20: the row is viewed as [N1][2^14].  Phase A transforms the
