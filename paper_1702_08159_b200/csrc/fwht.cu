@@ -22,8 +22,6 @@
 //               of <= 24 MiB keep phase A's output in the 126 MB L2 for
 //               phase B, which overlaps the next chunk's phase A on a side
 //               stream.
-//   (fwht_cluster_kernel, K = n/2^14 CTAs with DSMEM loads, is the round-1
-//   path for 2^15..2^17; kept for builds with -DMCK_FWHT_TMEM=0.)
 // parity variant (verification only; bit-exact to the reference on
 //   OpenBLAS SkylakeX): every aligned base chunk (256) becomes the sequential
 //   fp32 sum over k of H[k][j]*x_k, then combine stages (a+b, (a+b)-2b).
@@ -31,9 +29,7 @@
 #include "fwht_core.cuh"
 #include "umma.cuh"
 
-#include <cooperative_groups.h>
 
-namespace cg = cooperative_groups;
 
 namespace mck {
 
@@ -237,142 +233,14 @@ int launch_cols(V* data, int64_t rows, int logn1, int n2, cudaStream_t st) {
   }
 }
 
-// n = K * 2^14, K = 2..16 (fp32): one thread-block cluster of K CTAs per row,
-// a single HBM pass.  CTA c transforms its contiguous 2^14-segment with the
-// register/shared-memory kernel and parks the result in its shared memory;
-// after a cluster barrier it owns 1/K of the segment positions and applies
-// H_K across the K segments (segment index = the top log2 K index bits),
-// reading the peers' shared memory through DSMEM (16-byte loads) and writing
-// all K output segments of its share.  A second cluster barrier keeps every
-// CTA's shared memory alive until the peers have read it.
-#ifndef MCK_CLUSTER_MINB
-#define MCK_CLUSTER_MINB 3  // 40 registers: 3 CTAs per SM (2^15: 0.68 -> 0.73 of HBM)
-#endif
-template <int K>
-__global__ void __launch_bounds__(RowCfg<14, 5>::T, MCK_CLUSTER_MINB)
-fwht_cluster_kernel(float* __restrict__ data, int64_t rows) {
-  using C = RowCfg<14, 5>;
-  constexpr int VW = K >= 16 ? 2 : 4;  // K vectors in registers
-  constexpr int SEG = C::N, SHAREV = SEG / K / VW;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* s = reinterpret_cast<float*>(smem_raw);
-  cg::cluster_group cl = cg::this_cluster();
-  const unsigned c = cl.block_rank();
-  const int64_t row = blockIdx.x / K;
-  const uint32_t tid = threadIdx.x;
-  float* prow = data + row * (int64_t)(K * SEG);
-  float v[C::R];
-  load_row_L<C>(prow + (int64_t)c * SEG, tid, v);
-  butterflies<C::R, C::PL, C::PL>(v);
-  middle_rounds<C, 0, C::PL>(s, tid, 0, v);
-  // transform complete in layout PM, whose lanes run along index bits 0..4:
-  // scalar stores straight into the linear segment are conflict free
-  constexpr uint32_t PM = last_mid_regs<C>();
-  __syncthreads();
-  {
-    float* base = s + thread_part<C::FULL, PM>(tid);
-#pragma unroll
-    for (int k = 0; k < C::R; ++k) base[deposit_bits((uint32_t)k, PM)] = v[k];
-  }
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  using VT = typename VecT<float, VW>::T;
-  constexpr int ITER = (SHAREV + C::T - 1) / C::T;
-  VT a[ITER][K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const VT* seg = cl.map_shared_rank(reinterpret_cast<const VT*>(s), (unsigned)k) + c * SHAREV;
-#pragma unroll
-    for (int it = 0; it < ITER; ++it)
-      if (SHAREV % C::T == 0 || (int)tid + it * C::T < SHAREV) a[it][k] = seg[tid + it * C::T];
-  }
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-#pragma unroll
-    for (int h = 1; h < K; h <<= 1)
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (!(k & h)) vadd(a[it][k], a[it][k | h]);
-  }
-  // every remote load has been consumed: peers may release their shared
-  // memory once all CTAs arrive (the global stores overlap the barrier)
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-#pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int q = (int)tid + it * C::T;
-    if (SHAREV % C::T != 0 && q >= SHAREV) continue;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-      reinterpret_cast<VT*>(prow + (int64_t)k * SEG)[c * SHAREV + q] = a[it][k];
-  }
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-}
-
-template <int K>
-int launch_cluster_t(float* data, int64_t rows, cudaStream_t st) {
-  using C = RowCfg<14, 5>;
-  const size_t smem = (size_t)C::SMEM_FLOATS * sizeof(float);
-  auto kern = fwht_cluster_kernel<K>;
-  static PerDevice pd;
-  const DeviceSlot* ds = nullptr;
-  MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
-    MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem), "fwht cluster smem"));
-    if (K > 8)
-      MCK_TRY(check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-                         "fwht cluster size"));
-    return MCK_OK;
-  }));
-  for (int64_t r0 = 0; r0 < rows; r0 += (1ll << 26)) {
-    const int64_t nr = rows - r0 < (1ll << 26) ? rows - r0 : (1ll << 26);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(nr * K));
-    cfg.blockDim = dim3(C::T);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = K;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    MCK_TRY(check_cuda(cudaLaunchKernelEx(&cfg, kern, data + r0 * (int64_t)K * C::N, nr),
-                       "fwht_cluster_kernel launch"));
-  }
-  return check_launch("fwht_cluster_kernel");
-}
-
-// Rows of 2^logn with 15 <= logn <= 18 in one pass (fp32).
-int launch_cluster(float* data, int64_t rows, int logn, cudaStream_t st) {
-  switch (logn) {
-    case 15: return launch_cluster_t<2>(data, rows, st);
-    case 16: return launch_cluster_t<4>(data, rows, st);
-    case 17: return launch_cluster_t<8>(data, rows, st);
-    case 18: return launch_cluster_t<16>(data, rows, st);
-    default: return fail_value("internal: no cluster kernel for 2^%d", logn);
-  }
-}
-
-// n = NSEG * 2^14, NSEG = 2 or 4 (fp32): the whole row stays on ONE SM, one
-// HBM pass, no cluster.  A persistent CTA of 512 threads walks its rows; each
-// 2^14-segment goes through the register/shared-memory transform of the row
-// kernel and is then parked in tensor memory -- the CTA owns all of the SM's
-// TMEM (NSEG * 64 KB of the 256 KB), used here as a thread-private register
-// extension: thread t of warp w writes its 32 registers to TMEM lane
-// 32*(w%4)+t, columns (w/4)*32*NSEG + 32*s.  Every thread holds the same
-// positions of every segment, so H_NSEG across the segments needs no exchange
-// at all: read the NSEG segments' values back (tcgen05.ld), butterfly, store
-// 16 bytes per segment.  The next segment's global loads are issued into a
-// second register set before the current segment is transformed, across row
-// boundaries too, so HBM reads stay in flight under the arithmetic.
+// ---- tensor-memory kernels (2^15 .. 2^18, fp32).  A persistent 512-thread
+// CTA owns its SM's tensor memory (256 KB) and uses it as a thread-private
+// register extension: thread t of warp w reads / writes TMEM lane
+// 32*(w%4)+t, columns (w/4)*32*NSEG + ... (tcgen05.st / tcgen05.ld, 32 columns
+// per thread and 2^14 segment).  Every thread holds the same positions of
+// every segment, so H across the segments needs no exchange at all.
 #ifndef MCK_FWHT_TMEM
 #define MCK_FWHT_TMEM 1
-#endif
-#ifndef MCK_FWHT_2BUF
-#define MCK_FWHT_2BUF 1  // alternate two exchange buffers (one barrier per exchange)
-#endif
-#ifndef MCK_FWHT_TMEM_FIRST
-#define MCK_FWHT_TMEM_FIRST 1  // one-SM TMEM kernel with H_NSEG first (no store burst at the row end)
 #endif
 #ifndef MCK_FWHT_VIRTUAL
 #define MCK_FWHT_VIRTUAL 2  // largest row / 2^16 on the virtual-row kernel (2^17: 0.71 -> 0.82; 4 = 2^18 too: 0.45 vs 0.55 with DSMEM)
@@ -407,38 +275,6 @@ __device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, float (&v)[8]) {
 // segment -- or of segment 0 of `next` (may be null) -- fly meanwhile.
 constexpr int TMEM_S_FLOATS = (RowCfg<14, 5>::SMEM_FLOATS + 3) / 4 * 4;
 
-template <int NSEG>
-__device__ __forceinline__ void tmem_park_chunk(float* s, float* s2, uint32_t tid, uint32_t tbase,
-                                                const float* chunk, const float* next,
-                                                float (&w)[RowCfg<14, 5>::R]) {
-  using C = RowCfg<14, 5>;
-  float v[C::R];
-#pragma unroll
-  for (int sg = 0; sg < NSEG; ++sg) {
-#pragma unroll
-    for (int k = 0; k < C::R; ++k) v[k] = w[k];
-    if (sg + 1 < NSEG) {
-      load_row_L<C>(chunk + (int64_t)(sg + 1) * C::N, tid, w);
-    } else if (next) {
-      load_row_L<C>(next, tid, w);
-    }
-    butterflies<C::R, C::PL, C::PL>(v);
-    // ends in layout PM (lanes on index bits 0..4): parked as is, no
-    // exchange back to the 16-byte layout
-#if MCK_FWHT_2BUF
-    middle_rounds_2buf<C, 0, C::PL>(s, s2, tid, 0, v);
-#else
-    middle_rounds<C, 0, C::PL>(s, tid, 0, v);
-#endif
-    tmem_st32(tbase + 32u * sg, v, 0);
-    tmem_st32(tbase + 32u * sg + 16u, v, 16);
-    // re-align the warps: the next segment's loads then go out as one burst
-    // (measured: 2^15 0.83 -> 0.86 of HBM)
-    __syncthreads();
-  }
-  umma::tmem_wait_st();
-}
-
 // Eight parked registers (8j .. 8j+7) of every segment, H_NSEG applied.
 template <int NSEG>
 __device__ __forceinline__ void tmem_piece(uint32_t tbase, int j, float (&a)[NSEG][8]) {
@@ -455,53 +291,8 @@ __device__ __forceinline__ void tmem_piece(uint32_t tbase, int j, float (&a)[NSE
       }
 }
 
-template <int NSEG>
-__global__ void __launch_bounds__(RowCfg<14, 5>::T, 1)
-fwht_tmem_kernel(float* __restrict__ data, int64_t rows) {
-  using C = RowCfg<14, 5>;
-  constexpr int SEG = C::N;
-  constexpr uint32_t COLS = 32 * NSEG * (C::T / 128);  // 32 columns per thread and segment
-  static_assert(COLS <= 512 && (COLS & (COLS - 1)) == 0, "TMEM columns");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* s = reinterpret_cast<float*>(smem_raw);
-  __shared__ uint32_t tmem_slot;
-  const uint32_t tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) umma::tmem_alloc<COLS>(&tmem_slot);
-  umma::fence_before();
-  __syncthreads();
-  umma::fence_after();
-  const uint32_t tbase = tmem_slot + ((32u * (warp & 3u)) << 16) + (warp >> 2) * (32u * NSEG);
-
-  float w[C::R];
-  int64_t row = blockIdx.x;
-  if (row < rows) load_row_L<C>(data + row * (int64_t)(NSEG * SEG), tid, w);
-  for (; row < rows; row += gridDim.x) {
-    float* prow = data + row * (int64_t)(NSEG * SEG);
-    const int64_t nrow = row + gridDim.x;
-    tmem_park_chunk<NSEG>(s, s + TMEM_S_FLOATS, tid, tbase, prow, nrow < rows ? data + nrow * (int64_t)(NSEG * SEG) : nullptr, w);
-    // H_NSEG across the segments, 8 registers at a time; a warp instruction
-    // stores 128 contiguous bytes (register k of layout PM sits at element
-    // tpart | deposit(k, PM))
-    constexpr uint32_t PM = last_mid_regs<C>();
-    float* pt = prow + thread_part<C::FULL, PM>(tid);
-#pragma unroll
-    for (int j = 0; j < C::R / 8; ++j) {
-      float a[NSEG][8];
-      tmem_piece<NSEG>(tbase, j, a);
-#pragma unroll
-      for (int sg = 0; sg < NSEG; ++sg) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          pt[(int64_t)sg * SEG + deposit_bits((uint32_t)(8 * j + i), PM)] = a[sg][i];
-      }
-    }
-  }
-  umma::fence_before();
-  __syncthreads();
-  if (warp == 0) umma::tmem_free<COLS>(tmem_slot);
-}
-
-// Same row-on-one-SM transform with H_NSEG FIRST (the stages commute): the
+// n = NSEG * 2^14, NSEG = 2 or 4: the whole row on ONE SM, one HBM pass, no
+// cluster, with H_NSEG FIRST (the stages commute): the
 // row arrives in NSEG pieces -- registers j*32/NSEG .. of layout L of every
 // segment, prefetched one piece per segment step -- and each piece gets H_NSEG
 // across the segments before it is parked.  A segment step then reads one
@@ -729,11 +520,7 @@ int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   // per SM, which owns the TMEM
   const size_t smem = 2 * (size_t)TMEM_S_FLOATS * sizeof(float);
   static_assert(2 * (size_t)TMEM_S_FLOATS * sizeof(float) > 116 * 1024, "one CTA per SM");
-#if MCK_FWHT_TMEM_FIRST
   auto kern = fwht_tmem_first_kernel<NSEG>;
-#else
-  auto kern = fwht_tmem_kernel<NSEG>;
-#endif
   static PerDevice pd;
   const DeviceSlot* ds = nullptr;
   MCK_TRY(per_device(pd, &ds, [&](int, DeviceSlot&) {
@@ -744,7 +531,7 @@ int launch_tmem_t(float* data, int64_t rows, cudaStream_t st) {
   int64_t grid = ds->sms;
   if (grid > rows) grid = rows;
   kern<<<(unsigned)grid, C::T, smem, st>>>(data, rows);
-  return check_launch("fwht_tmem_kernel");
+  return check_launch("fwht_tmem_first_kernel");
 }
 
 // n = K * 2^16, K = 2..16 (fp32): one cluster of K CTAs per row, one HBM
@@ -1303,8 +1090,6 @@ int fwht_fast(V* data, int64_t rows, int64_t n, cudaStream_t st) {
       const int rc = launch_tmem_cluster(data, rows, logn, st);
       if (rc != kNoClusterFits) return rc;
     }
-#else
-    if (logn >= 15 && logn <= 17) return launch_cluster(data, rows, logn, st);
 #endif
   }
   if (logn <= max_row_logn) return launch_rows_by_logn<V>(data, rows, logn, st);
